@@ -1,0 +1,280 @@
+"""paper_2109_00626_b200 -- batched Tensor-Train contraction (TTCP, arXiv 2109.00626) on B200.
+
+Thin Python binding over the C ABI of libttc.so (include/ttc.h): the functions here carry the C names and
+only marshal arguments (torch tensors -> device pointers, numpy -> host pointers, torch stream -> handle).
+Every step of the computation runs in the CUDA kernels of libttc.so; there is no CPU fallback, and
+importing this package without the built library raises.
+
+    X = TTDevice(cores, dims, ranks=None or int32[B, N+1], offsets=None or int64[B])
+    out = ttc_inner(X, Y)                                  # <X_b, Y_b>, float32 [B] on the device
+    plan = ttc_contract_plan_create(X, Y, [2, 4, 6], [1, 3, 5])
+    order, dims, src, perm, total, max_rank = ttc_contract_plan_query(plan)
+    cores, ranks, offsets = ttc_contract(plan, X, Y)       # output TTs (ladder order; perm -> Eq. 8 order)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libttc.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+                      "there is no fallback implementation")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+TTC_OK, TTC_ERR_NULL, TTC_ERR_SHAPE, TTC_ERR_RANK, TTC_ERR_MODES = 0, 1, 2, 3, 4
+TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG = 5, 6, 7, 8, 9
+TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
+
+EXPORTED = ("ttc_inner", "ttc_contract_plan_create", "ttc_contract_plan_query", "ttc_contract_plan_layout",
+            "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
+            "ttc_last_error", "ttc_version")
+
+
+class ttc_tt_batch(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("order", ctypes.c_int32), ("dims", ctypes.c_void_p),
+                ("ranks_host", ctypes.c_void_p), ("ranks_dev", ctypes.c_void_p), ("uniform_rank", ctypes.c_int32),
+                ("offsets_host", ctypes.c_void_p), ("offsets_dev", ctypes.c_void_p), ("cores", ctypes.c_void_p),
+                ("n_elems", ctypes.c_int64)]
+
+
+_P = ctypes.POINTER
+_lib.ttc_inner.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_contract_plan_create.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_int32, ctypes.c_void_p,
+                                          ctypes.c_void_p, _P(ctypes.c_void_p)]
+_lib.ttc_contract_plan_query.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 6
+_lib.ttc_contract_plan_layout.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_contract.argtypes = [ctypes.c_void_p, _P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p]
+_lib.ttc_contract_plan_destroy.argtypes = [ctypes.c_void_p]
+_lib.ttc_contract_plan_destroy.restype = None
+_lib.ttc_pair_cost.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_partition.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+_lib.ttc_status_string.restype = ctypes.c_char_p
+_lib.ttc_status_string.argtypes = [ctypes.c_int]
+_lib.ttc_last_error.restype = ctypes.c_char_p
+_lib.ttc_version.restype = ctypes.c_int32
+for _f in ("ttc_inner", "ttc_contract_plan_create", "ttc_contract_plan_query", "ttc_contract_plan_layout",
+           "ttc_contract", "ttc_pair_cost", "ttc_partition"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+
+class TTCError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        super().__init__(f"{ttc_status_string(status)}: {detail}")
+
+
+def ttc_status_string(status: int) -> str:
+    return _lib.ttc_status_string(int(status)).decode()
+
+
+def ttc_last_error() -> str:
+    return _lib.ttc_last_error().decode()
+
+
+def ttc_version() -> int:
+    return int(_lib.ttc_version())
+
+
+def _check(rc: int):
+    if rc != TTC_OK:
+        raise TTCError(rc, ttc_last_error())
+
+
+def _ptr(a) -> Optional[int]:
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+class TTDevice:
+    """A batch of B trains as the C ABI sees it (ttc_tt_batch), with the host arrays it needs kept alive.
+
+    cores: float32 torch tensor (flat, on the GPU for compute calls); dims: (I_1..I_N);
+    ranks: int32 [B, N+1] (row b = R_0..R_N) or None with uniform_rank; offsets: int64 [B] or None (packed).
+    Ranks that are the same for every train are passed as uniform (the C ABI's fast path)."""
+
+    def __init__(self, cores: torch.Tensor, dims: Sequence[int], ranks=None, offsets=None, uniform_rank: int = None,
+                 batch: int = None):
+        if cores.dtype != torch.float32:
+            raise TypeError("cores must be float32")
+        if not cores.is_contiguous():
+            raise ValueError("cores must be contiguous")
+        self.cores = cores
+        self.dims_np = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
+        N = int(self.dims_np.shape[0])
+        self.ranks_np = None
+        self.uniform_rank = 1
+        if ranks is not None:
+            r = np.ascontiguousarray(np.asarray(ranks, dtype=np.int32))
+            if r.ndim != 2 or r.shape[1] != N + 1:
+                raise ValueError(f"ranks must be [B, N+1] = [*, {N + 1}], got {r.shape}")
+            B = r.shape[0]
+            inner = r[:, 1:N]
+            uni = B > 0 and N > 1 and bool(np.all(inner == inner.flat[0])) and bool(np.all(r[:, 0] == 1)) \
+                and bool(np.all(r[:, N] == 1))
+            if B > 0 and N == 1 and bool(np.all(r == 1)):
+                uni, self.uniform_rank = True, 1
+            elif uni:
+                self.uniform_rank = int(inner.flat[0])
+            if not uni:
+                self.ranks_np = r
+        else:
+            if batch is None:
+                raise ValueError("batch is required with uniform ranks")
+            B = int(batch)
+            self.uniform_rank = int(uniform_rank if uniform_rank is not None else 1)
+        self.B = int(B)
+        self.N = N
+        self.offsets_np = None
+        if offsets is not None:
+            o = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+            if o.shape != (B,):
+                raise ValueError(f"offsets must be [B] = [{B}], got {o.shape}")
+            packed = self._packed_offsets()
+            if packed is None or not np.array_equal(o, packed):
+                self.offsets_np = o
+        dev = cores.device
+        self.ranks_dev = torch.from_numpy(self.ranks_np).to(dev) if self.ranks_np is not None else None
+        self.offsets_dev = torch.from_numpy(self.offsets_np).to(dev) if self.offsets_np is not None else None
+        if self.ranks_np is not None and self.offsets_np is None and self.B > 1:
+            self.offsets_np = self._packed_offsets()
+            self.offsets_dev = torch.from_numpy(self.offsets_np).to(dev)
+        self.c = ttc_tt_batch(self.B, self.N, _ptr(self.dims_np), _ptr(self.ranks_np), _ptr(self.ranks_dev),
+                              self.uniform_rank, _ptr(self.offsets_np), _ptr(self.offsets_dev),
+                              cores.data_ptr() if cores.numel() else None, int(cores.numel()))
+
+    def _packed_offsets(self):
+        if self.ranks_np is None:
+            return None if self.B == 0 else np.arange(self.B, dtype=np.int64) * self._uniform_train_elems()
+        r = self.ranks_np.astype(np.int64)
+        sizes = (r[:, :-1] * self.dims_np[None, :].astype(np.int64) * r[:, 1:]).sum(axis=1)
+        offs = np.zeros(self.B, np.int64)
+        if self.B > 1:
+            offs[1:] = np.cumsum(sizes)[:-1]
+        return offs
+
+    def _uniform_train_elems(self):
+        r = [1] + [self.uniform_rank] * (self.N - 1) + [1]
+        return int(sum(r[n] * int(self.dims_np[n]) * r[n + 1] for n in range(self.N)))
+
+    @classmethod
+    def from_batch(cls, b, device=None):
+        """From any object with .cores, .dims, .ranks, .offsets (e.g. ttgen.TTBatch)."""
+        cores = b.cores if device is None else b.cores.to(device)
+        return cls(cores.contiguous(), b.dims, ranks=b.ranks, offsets=b.offsets)
+
+    def rank_rows(self) -> np.ndarray:
+        if self.ranks_np is not None:
+            return self.ranks_np
+        r = np.full((self.B, self.N + 1), self.uniform_rank, np.int32)
+        r[:, 0] = 1
+        r[:, self.N] = 1
+        return r
+
+
+def _stream_handle(stream) -> Optional[int]:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def ttc_inner(x: TTDevice, y: TTDevice, out: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """out[b] = <X_b, Y_b> (ttc.h: ttc_inner).  Asynchronous on `stream` (default: torch's current stream)."""
+    if out is None:
+        out = torch.empty(x.B, dtype=torch.float32, device=x.cores.device)
+    _check(_lib.ttc_inner(ctypes.byref(x.c), ctypes.byref(y.c), _ptr(out) if out.numel() else None,
+                          _stream_handle(stream)))
+    return out
+
+
+class ContractPlan:
+    """Owns a ttc_contract_plan* (host-only)."""
+
+    def __init__(self, handle: int, x: TTDevice, y: TTDevice):
+        self.handle = handle
+        order = ctypes.c_int32(0)
+        total = ctypes.c_int64(0)
+        mr = ctypes.c_int32(0)
+        L = x.N + y.N
+        dims, src, perm = (np.zeros(max(L, 1), np.int32) for _ in range(3))
+        _check(_lib.ttc_contract_plan_query(handle, ctypes.byref(order), _ptr(dims), _ptr(src), _ptr(perm),
+                                            ctypes.byref(total), ctypes.byref(mr)))
+        self.L = order.value
+        self.dims, self.src, self.perm = dims[:self.L].copy(), src[:self.L].copy(), perm[:self.L].copy()
+        self.total = total.value
+        self.max_rank = mr.value
+        self.B = x.B
+        self.ranks = np.zeros((x.B, self.L + 1), np.int32)
+        self.offsets = np.zeros(x.B, np.int64)
+        _check(_lib.ttc_contract_plan_layout(handle, _ptr(self.ranks) if x.B else None,
+                                             _ptr(self.offsets) if x.B else None))
+        self._offsets_dev = None
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.ttc_contract_plan_destroy(self.handle)
+            self.handle = None
+
+
+def ttc_contract_plan_create(x: TTDevice, y: TTDevice, x_modes: Sequence[int], y_modes: Sequence[int]) -> ContractPlan:
+    xm = np.ascontiguousarray(np.asarray(list(x_modes), dtype=np.int32))
+    ym = np.ascontiguousarray(np.asarray(list(y_modes), dtype=np.int32))
+    h = ctypes.c_void_p(0)
+    _check(_lib.ttc_contract_plan_create(ctypes.byref(x.c), ctypes.byref(y.c), len(xm), _ptr(xm) if len(xm) else None,
+                                         _ptr(ym) if len(ym) else None, ctypes.byref(h)))
+    return ContractPlan(h.value, x, y)
+
+
+def ttc_contract_plan_query(plan: ContractPlan):
+    return plan.L, plan.dims, plan.src, plan.perm, plan.total, plan.max_rank
+
+
+def ttc_contract_plan_layout(plan: ContractPlan):
+    return plan.ranks, plan.offsets
+
+
+def ttc_contract_plan_destroy(plan: ContractPlan):
+    plan.__del__()
+
+
+def ttc_contract(plan: ContractPlan, x: TTDevice, y: TTDevice, out: torch.Tensor = None, stream=None):
+    """Output cores of every pair (ttc.h: ttc_contract) -> (cores float32 [total], ranks [B, L+1], offsets [B])."""
+    if out is None:
+        out = torch.empty(max(plan.total, 0), dtype=torch.float32, device=x.cores.device)
+    uniform_out = plan.B <= 1 or bool(np.all(plan.ranks == plan.ranks[0:1]))
+    offs_dev = None
+    if not uniform_out:
+        if plan._offsets_dev is None or plan._offsets_dev.device != out.device:
+            plan._offsets_dev = torch.from_numpy(plan.offsets).to(out.device)
+        offs_dev = plan._offsets_dev
+    _check(_lib.ttc_contract(plan.handle, ctypes.byref(x.c), ctypes.byref(y.c), _ptr(out) if out.numel() else None,
+                             _ptr(offs_dev), _stream_handle(stream)))
+    return out, plan.ranks, plan.offsets
+
+
+def ttc_pair_cost(x: TTDevice, y: TTDevice):
+    """Host cost model (ttc.h): per pair sweep MACs and algorithmic HBM bytes."""
+    mac = np.zeros(x.B, np.float64)
+    by = np.zeros(x.B, np.float64)
+    _check(_lib.ttc_pair_cost(ctypes.byref(x.c), ctypes.byref(y.c), _ptr(mac) if x.B else None,
+                              _ptr(by) if x.B else None))
+    return mac, by
+
+
+def ttc_partition(cost, k: int) -> np.ndarray:
+    """Contiguous k-way split of the batch minimising the largest part cost (ttc.h)."""
+    c = np.ascontiguousarray(np.asarray(cost, dtype=np.float64))
+    bounds = np.zeros(k + 1, np.int32)
+    _check(_lib.ttc_partition(_ptr(c) if c.size else None, int(c.size), int(k), _ptr(bounds)))
+    return bounds

@@ -1,0 +1,277 @@
+// contract.cu -- batched ladder tt_contract (ttc.h; Alg. 2 steps 4-6, generalised to K
+// disjoint non-crossing mode pairs, readings R7-R10).  One CTA per pair.
+//
+// Per pair: (1) transfers T_k[(r + R p), (r' + R' p')] = sum_i X_{n_k}[r,i,r'] Y_{m_k}[p,i,p'] (the paper's
+// K = A_x^T A_y generalised, Eq. 12) and products of consecutive transfers are formed in shared memory;
+// (2) every output core is streamed to HBM in Eq. 2 order.  Free cores are Kronecker products with an
+// identity (X_n (x) I_P or I_R (x) Y_m): their zeros are generated in registers, never read, and the
+// absorbed transfer is applied structure-aware (sum over the non-identity bond only).  The kernel is
+// bound by the output writes (output >> input), so stores are 16-byte streaming stores (st.global.cs).
+#include "ttc_internal.h"
+
+namespace ttc {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct PairCtx {
+    int32_t rx[kMaxContractOrder + 1], ry[kMaxContractOrder + 1];
+    int64_t xo[kMaxContractOrder + 1], yo[kMaxContractOrder + 1];   // core offsets within the train
+    int32_t orr[kMaxLadder + 1];                                     // output bond ranks
+    int64_t oo[kMaxLadder + 1];                                      // output core offsets within the pair
+};
+
+__device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void st_cs1(float* p, float a) {
+    asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+
+// T_k (rows = R_{n-1} P_{m-1}, cols = R_n P_m) into dst, column-major.
+__device__ void build_transfer(const ContractArgs& a, const PairCtx& c, const float* xc, const float* yc,
+                               const LadderEl& el, float* dst) {
+    const int n = el.mode, m = el.hold;
+    const int R = c.rx[n], Rn = c.rx[n + 1], P = c.ry[m], Pn = c.ry[m + 1], I = a.xdims[n];
+    const float* X = xc + c.xo[n];
+    const float* Y = yc + c.yo[m];
+    const int rows = R * P, total = rows * Rn * Pn;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int row = e % rows, col = e / rows;
+        const int r = row % R, p = row / R, rr = col % Rn, pp = col / Rn;
+        float acc = 0.0f;
+        for (int i = 0; i < I; ++i)
+            acc = fmaf(__ldg(X + r + R * (i + I * rr)), __ldg(Y + p + P * (i + I * pp)), acc);
+        dst[e] = acc;
+    }
+}
+
+// C (m x n) = A (m x k) * B (k x n), column-major, shared memory.
+__device__ void smem_matmul(const float* A, const float* B, float* C, int m, int k, int n) {
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+        const int i = e % m, j = e / m;
+        float acc = 0.0f;
+        for (int l = 0; l < k; ++l) acc = fmaf(A[i + m * l], B[l + k * j], acc);
+        C[e] = acc;
+    }
+}
+
+// Product of `count` consecutive transfers starting at sequence index `first` into dst; returns rows/cols.
+__device__ void build_chain(const ContractArgs& a, const PairCtx& c, const float* xc, const float* yc, int first,
+                            int count, float* dst, float* tmp, int* rows_out, int* cols_out) {
+    const LadderEl& e0 = a.seq[first];
+    const int rows = c.rx[e0.mode] * c.ry[e0.hold];
+    int cols = c.rx[e0.mode + 1] * c.ry[e0.hold + 1];
+    if (count == 1) {
+        build_transfer(a, c, xc, yc, e0, dst);
+    } else {
+        float* cur = tmp;
+        float* nxt = tmp + a.tmp_size;
+        float* prod = tmp + 2 * a.tmp_size;
+        build_transfer(a, c, xc, yc, e0, cur);
+        for (int t = 1; t < count; ++t) {
+            const LadderEl& et = a.seq[first + t];
+            __syncthreads();
+            build_transfer(a, c, xc, yc, et, nxt);
+            __syncthreads();
+            const int kk = cols;
+            const int nn = c.rx[et.mode + 1] * c.ry[et.hold + 1];
+            float* target = (t == count - 1) ? dst : prod;
+            smem_matmul(cur, nxt, target, rows, kk, nn);
+            cols = nn;
+            if (t != count - 1) { float* sw = cur; cur = prod; prod = sw; }
+        }
+    }
+    *rows_out = rows;
+    *cols_out = cols;
+}
+
+// Geometry of one free core before absorption.
+struct FreeCore {
+    bool xfree;
+    const float* G;   // source core values
+    int Rb;           // XFREE: R (X left bond);  YFREE: P (Y left bond)
+    int Rn;           // XFREE: R' (X right bond); YFREE: P'
+    int H;            // carried identity size: XFREE: P_b;  YFREE: R_a
+    int I;            // mode size
+    int Ain, Bin;     // rows / cols before absorption: XFREE (R H, R' H), YFREE (H P, H P')
+};
+
+// Value of the (left-absorbed or plain) core at (alpha, i, gamma); gamma indexes the pre-absorption cols.
+__device__ __forceinline__ float cprime(const FreeCore& f, const float* TL, int Aout, bool has_tl, int alpha, int i,
+                                        int gamma) {
+    if (f.xfree) {   // [r + R p, i, r' + R' p'] = X[r, i, r'] delta_{p p'}
+        const int rr = gamma % f.Rn, pp = gamma / f.Rn;
+        const float* col = f.G + f.Rb * (i + f.I * rr);
+        if (has_tl) {
+            float acc = 0.0f;
+            for (int r = 0; r < f.Rb; ++r) acc = fmaf(TL[alpha + Aout * (r + f.Rb * pp)], __ldg(col + r), acc);
+            return acc;
+        }
+        const int r = alpha - f.Rb * pp;
+        return (r >= 0 && r < f.Rb) ? __ldg(col + r) : 0.0f;
+    } else {         // [r + H p, j, r' + H p'] = delta_{r r'} Y[p, j, p']
+        const int rr = gamma % f.H, pp = gamma / f.H;
+        const float* col = f.G + f.Rb * (i + f.I * pp);
+        if (has_tl) {
+            float acc = 0.0f;
+            for (int p = 0; p < f.Rb; ++p) acc = fmaf(TL[alpha + Aout * (rr + f.H * p)], __ldg(col + p), acc);
+            return acc;
+        }
+        const int d = alpha - rr;
+        if (d < 0 || d % f.H) return 0.0f;
+        const int p = d / f.H;
+        return p < f.Rb ? __ldg(col + p) : 0.0f;
+    }
+}
+
+__device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* xc, const float* yc, int l,
+                          const float* TL, const float* TR, float* out) {
+    const OutCore& oc = a.outc[l];
+    const LadderEl& el = a.seq[oc.el];
+    FreeCore f;
+    f.xfree = el.kind == EL_XFREE;
+    if (f.xfree) {
+        f.G = xc + c.xo[el.mode];
+        f.Rb = c.rx[el.mode]; f.Rn = c.rx[el.mode + 1]; f.H = c.ry[el.hold]; f.I = a.xdims[el.mode];
+        f.Ain = f.Rb * f.H; f.Bin = f.Rn * f.H;
+    } else {
+        f.G = yc + c.yo[el.mode];
+        f.Rb = c.ry[el.mode]; f.Rn = c.ry[el.mode + 1]; f.H = c.rx[el.hold]; f.I = a.ydims[el.mode];
+        f.Ain = f.H * f.Rb; f.Bin = f.H * f.Rn;
+    }
+    const bool has_tl = oc.lt_count > 0, has_tr = oc.rt_count > 0;
+    const int Aout = c.orr[l], Bout = c.orr[l + 1];
+    const int I = f.I;
+    const int64_t total = (int64_t)Aout * I * Bout;
+    float* dst = out + c.oo[l];
+    const bool quad_ok = (Aout % 4 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+    if (!has_tr && quad_ok) {
+        // 4 consecutive alpha of one column per thread -> one 16-byte streaming store
+        const int qpc = Aout / 4;
+        const int64_t nq = total / 4;
+        for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
+            const int col = (int)(q / qpc);
+            const int a0 = (int)(q - (int64_t)col * qpc) * 4;
+            const int i = col % I, beta = col / I;
+            float v[4];
+            if (f.xfree) {
+                const int rr = beta % f.Rn, pp = beta / f.Rn;
+                const float* gcol = f.G + f.Rb * (i + I * rr);
+                if (has_tl) {
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float* tl = TL + a0 + Aout * (f.Rb * pp);
+                    for (int r = 0; r < f.Rb; ++r) {
+                        const float g = __ldg(gcol + r);
+                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * r);
+                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
+                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
+                    }
+                    v[0] = acc.x; v[1] = acc.y; v[2] = acc.z; v[3] = acc.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int r = a0 + k - f.Rb * pp;
+                        v[k] = (r >= 0 && r < f.Rb) ? __ldg(gcol + r) : 0.0f;
+                    }
+                }
+            } else {
+                const int rr = beta % f.H, pp = beta / f.H;
+                const float* gcol = f.G + f.Rb * (i + I * pp);
+                if (has_tl) {
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float* tl = TL + a0 + Aout * rr;
+                    for (int p = 0; p < f.Rb; ++p) {
+                        const float g = __ldg(gcol + p);
+                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * f.H * p);
+                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
+                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
+                    }
+                    v[0] = acc.x; v[1] = acc.y; v[2] = acc.z; v[3] = acc.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int d = a0 + k - rr;
+                        const int p = d / f.H;
+                        v[k] = (d >= 0 && d - p * f.H == 0 && p < f.Rb) ? __ldg(gcol + p) : 0.0f;
+                    }
+                }
+            }
+            st_cs4(dst + 4 * q, v[0], v[1], v[2], v[3]);
+        }
+        return;
+    }
+    // general element path (right absorption, unaligned or odd row counts)
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+        const int alpha = (int)(e % Aout);
+        const int64_t col = e / Aout;
+        const int i = (int)(col % I), beta = (int)(col / I);
+        float v;
+        if (has_tr) {
+            v = 0.0f;
+            for (int g = 0; g < f.Bin; ++g) v = fmaf(cprime(f, TL, Aout, has_tl, alpha, i, g), TR[g + f.Bin * beta], v);
+        } else {
+            v = cprime(f, TL, Aout, has_tl, alpha, i, beta);
+        }
+        st_cs1(dst + e, v);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) contract_kernel(const ContractArgs a) {
+    extern __shared__ float scratch[];
+    __shared__ PairCtx c;
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        for (int n = 0; n <= a.N; ++n)
+            c.rx[n] = a.x.ranks ? a.x.ranks[(int64_t)b * (a.N + 1) + n] : ((n == 0 || n == a.N) ? 1 : a.x.urank);
+        for (int m = 0; m <= a.M; ++m)
+            c.ry[m] = a.y.ranks ? a.y.ranks[(int64_t)b * (a.M + 1) + m] : ((m == 0 || m == a.M) ? 1 : a.y.urank);
+        c.xo[0] = 0;
+        for (int n = 0; n < a.N; ++n) c.xo[n + 1] = c.xo[n] + (int64_t)c.rx[n] * a.xdims[n] * c.rx[n + 1];
+        c.yo[0] = 0;
+        for (int m = 0; m < a.M; ++m) c.yo[m + 1] = c.yo[m] + (int64_t)c.ry[m] * a.ydims[m] * c.ry[m + 1];
+        // output bond ranks: the right bond of each output core; first and last are 1
+        c.orr[0] = 1;
+        for (int l = 0; l < a.L; ++l) {
+            const LadderEl& el = a.seq[a.outc[l].el];
+            c.orr[l + 1] = el.kind == EL_XFREE ? c.rx[el.mode + 1] * c.ry[el.hold] : c.rx[el.hold] * c.ry[el.mode + 1];
+        }
+        c.orr[a.L] = 1;
+        c.oo[0] = 0;
+        for (int l = 0; l < a.L; ++l) {
+            const LadderEl& el = a.seq[a.outc[l].el];
+            const int I = el.kind == EL_XFREE ? a.xdims[el.mode] : a.ydims[el.mode];
+            c.oo[l + 1] = c.oo[l] + (int64_t)c.orr[l] * I * c.orr[l + 1];
+        }
+    }
+    __syncthreads();
+    const float* xc = a.x.cores + (a.x.offsets ? a.x.offsets[b] : (int64_t)b * a.x.train_elems);
+    const float* yc = a.y.cores + (a.y.offsets ? a.y.offsets[b] : (int64_t)b * a.y.train_elems);
+    float* out = a.out + (a.out_offsets ? a.out_offsets[b] : (int64_t)b * a.out_pair_elems);
+    float* TL = scratch + a.tl_off;
+    float* TR = scratch + a.tr_off;
+    float* tmp = scratch + a.tmp_off;
+    for (int l = 0; l < a.L; ++l) {
+        const OutCore& oc = a.outc[l];
+        int rows, cols;
+        if (oc.lt_count > 0) build_chain(a, c, xc, yc, oc.lt_first, oc.lt_count, TL, tmp, &rows, &cols);
+        if (oc.rt_count > 0) {
+            __syncthreads();
+            build_chain(a, c, xc, yc, oc.rt_first, oc.rt_count, TR, tmp, &rows, &cols);
+        }
+        __syncthreads();
+        emit_core(a, c, xc, yc, l, TL, TR, out);
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_contract(const ContractArgs& a, size_t smem_bytes, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+    contract_kernel<<<a.B, kThreads, smem_bytes, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ttc

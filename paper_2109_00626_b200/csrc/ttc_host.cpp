@@ -1,0 +1,518 @@
+// ttc_host.cpp -- the C ABI of libttc.so (include/ttc.h): host-side validation, planning, cost model,
+// partitioner and kernel dispatch.  Host data only until the final launch; no device allocation.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ttc_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ttc_status fail(ttc_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+bool mul_ok(int64_t a, int64_t b, int64_t* out) { return !__builtin_mul_overflow(a, b, out); }
+bool add_ok(int64_t a, int64_t b, int64_t* out) { return !__builtin_add_overflow(a, b, out); }
+
+// Host view of one validated operand batch.
+struct HostTrain {
+    const ttc_tt_batch* t = nullptr;
+    int B = 0, N = 0;
+    bool uniform = true;
+    int urank = 1;
+    int max_rank = 1;
+    int64_t train_elems_uniform = 0;   // uniform ranks: elements per train
+
+    int rank(int b, int n) const {
+        if (!uniform) return t->ranks_host[(int64_t)b * (N + 1) + n];
+        return (n == 0 || n == N) ? 1 : urank;
+    }
+};
+
+// A1: validate one operand batch; `name` is "X" or "Y".
+ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, HostTrain* h) {
+    if (!t) return fail(TTC_ERR_NULL, "%s: batch descriptor is NULL", name);
+    if (t->batch < 0) return fail(TTC_ERR_ARG, "%s: batch = %d < 0", name, t->batch);
+    if (t->order < 1) return fail(TTC_ERR_SHAPE, "%s: order N = %d < 1", name, t->order);
+    if (t->order > max_order)
+        return fail(TTC_ERR_UNSUPPORTED, "%s: order N = %d > %d supported", name, t->order, max_order);
+    if (!t->dims) return fail(TTC_ERR_NULL, "%s: dims is NULL", name);
+    h->t = t;
+    h->B = t->batch;
+    h->N = t->order;
+    for (int n = 0; n < t->order; ++n)
+        if (t->dims[n] < 1) return fail(TTC_ERR_SHAPE, "%s: mode %d has I = %d < 1", name, n + 1, t->dims[n]);
+    h->uniform = (t->ranks_host == nullptr);
+    if (h->uniform) {
+        if (t->ranks_dev)
+            return fail(TTC_ERR_ARG, "%s: ranks_dev given without ranks_host", name);
+        if (t->order > 1) {
+            if (t->uniform_rank < 1) return fail(TTC_ERR_RANK, "%s: uniform_rank = %d < 1", name, t->uniform_rank);
+            if (t->uniform_rank > TTC_MAX_RANK)
+                return fail(TTC_ERR_UNSUPPORTED, "%s: uniform_rank = %d > %d", name, t->uniform_rank, TTC_MAX_RANK);
+            h->urank = t->uniform_rank;
+        }
+        h->max_rank = t->order > 1 ? h->urank : 1;
+    } else {
+        if (t->batch > 0 && !t->ranks_dev) return fail(TTC_ERR_NULL, "%s: ranks_host given but ranks_dev is NULL", name);
+        int mr = 1;
+        for (int b = 0; b < t->batch; ++b) {
+            const int32_t* r = t->ranks_host + (int64_t)b * (t->order + 1);
+            if (r[0] != 1 || r[t->order] != 1)
+                return fail(TTC_ERR_RANK, "%s pair %d: boundary ranks R_0 = %d, R_N = %d (must be 1)", name, b, r[0],
+                            r[t->order]);
+            for (int n = 1; n < t->order; ++n) {
+                if (r[n] < 1) return fail(TTC_ERR_RANK, "%s pair %d: rank R_%d = %d < 1", name, b, n, r[n]);
+                if (r[n] > TTC_MAX_RANK)
+                    return fail(TTC_ERR_UNSUPPORTED, "%s pair %d: rank R_%d = %d > %d", name, b, n, r[n], TTC_MAX_RANK);
+                mr = std::max(mr, (int)r[n]);
+            }
+        }
+        h->max_rank = mr;
+    }
+    if (t->offsets_host && t->batch > 0 && !t->offsets_dev)
+        return fail(TTC_ERR_NULL, "%s: offsets_host given but offsets_dev is NULL", name);
+    if (!t->offsets_host && t->offsets_dev) return fail(TTC_ERR_ARG, "%s: offsets_dev given without offsets_host", name);
+    if (!t->offsets_host && !h->uniform && t->batch > 1)
+        return fail(TTC_ERR_ARG, "%s: heterogeneous ranks need explicit offsets", name);
+    if (t->batch > 0 && !t->cores) return fail(TTC_ERR_NULL, "%s: cores is NULL", name);
+    if (t->cores && (reinterpret_cast<uintptr_t>(t->cores) & 3u))
+        return fail(TTC_ERR_ALIGN, "%s: cores pointer not 4-byte aligned", name);
+    // sizes and bounds, overflow-checked
+    int64_t packed_end = 0;
+    for (int b = 0; b < t->batch; ++b) {
+        int64_t elems = 0;
+        if (b == 0 || !h->uniform) {
+            for (int n = 0; n < t->order; ++n) {
+                int64_t sz;
+                if (!mul_ok((int64_t)h->rank(b, n) * t->dims[n], h->rank(b, n + 1), &sz) || !add_ok(elems, sz, &elems))
+                    return fail(TTC_ERR_OVERFLOW, "%s pair %d: train size overflows int64", name, b);
+            }
+            if (h->uniform) h->train_elems_uniform = elems;
+        } else {
+            elems = h->train_elems_uniform;
+        }
+        int64_t start = t->offsets_host ? t->offsets_host[b] : packed_end, end;
+        if (start < 0) return fail(TTC_ERR_OVERFLOW, "%s pair %d: offset %lld < 0", name, b, (long long)start);
+        if (!add_ok(start, elems, &end)) return fail(TTC_ERR_OVERFLOW, "%s pair %d: offset + size overflows", name, b);
+        if (t->n_elems > 0 && end > t->n_elems)
+            return fail(TTC_ERR_OVERFLOW, "%s pair %d: train [%lld, %lld) runs past n_elems = %lld", name, b,
+                        (long long)start, (long long)end, (long long)t->n_elems);
+        packed_end = end;
+        if (!t->offsets_host && h->uniform && t->batch > 1) {
+            // packed uniform: the last train bounds everything
+            int64_t last;
+            if (!mul_ok(elems, t->batch, &last)) return fail(TTC_ERR_OVERFLOW, "%s: batch size overflows", name);
+            if (t->n_elems > 0 && last > t->n_elems)
+                return fail(TTC_ERR_OVERFLOW, "%s: %d packed trains of %lld floats exceed n_elems = %lld", name,
+                            t->batch, (long long)elems, (long long)t->n_elems);
+            break;
+        }
+    }
+    return TTC_OK;
+}
+
+ttc::TrainDev to_dev(const HostTrain& h) {
+    ttc::TrainDev d;
+    d.cores = h.t->cores;
+    d.ranks = h.uniform ? nullptr : h.t->ranks_dev;
+    d.offsets = h.t->offsets_host ? h.t->offsets_dev : nullptr;
+    d.urank = h.urank;
+    d.train_elems = h.train_elems_uniform;
+    return d;
+}
+
+ttc_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(TTC_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+}  // namespace
+
+// ================================================================================================ C ABI
+extern "C" {
+
+const char* ttc_status_string(ttc_status s) {
+    switch (s) {
+        case TTC_OK: return "TTC_OK";
+        case TTC_ERR_NULL: return "TTC_ERR_NULL";
+        case TTC_ERR_SHAPE: return "TTC_ERR_SHAPE";
+        case TTC_ERR_RANK: return "TTC_ERR_RANK";
+        case TTC_ERR_MODES: return "TTC_ERR_MODES";
+        case TTC_ERR_ALIGN: return "TTC_ERR_ALIGN";
+        case TTC_ERR_OVERFLOW: return "TTC_ERR_OVERFLOW";
+        case TTC_ERR_UNSUPPORTED: return "TTC_ERR_UNSUPPORTED";
+        case TTC_ERR_CUDA: return "TTC_ERR_CUDA";
+        case TTC_ERR_ARG: return "TTC_ERR_ARG";
+    }
+    return "TTC_ERR_UNKNOWN";
+}
+
+const char* ttc_last_error(void) { return g_last_error.c_str(); }
+
+int32_t ttc_version(void) { return TTC_VERSION_MAJOR * 100 + TTC_VERSION_MINOR; }
+
+ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_dev, void* stream) {
+    g_last_error.clear();
+    HostTrain hx, hy;
+    ttc_status st;
+    if ((st = check_batch(x, "X", TTC_MAX_ORDER, &hx)) != TTC_OK) return st;
+    if ((st = check_batch(y, "Y", TTC_MAX_ORDER, &hy)) != TTC_OK) return st;
+    if (x->batch != y->batch) return fail(TTC_ERR_SHAPE, "batch mismatch: X has %d trains, Y has %d", x->batch, y->batch);
+    if (x->order != y->order) return fail(TTC_ERR_SHAPE, "order mismatch: X N = %d, Y N = %d", x->order, y->order);
+    for (int n = 0; n < x->order; ++n)
+        if (x->dims[n] != y->dims[n])
+            return fail(TTC_ERR_SHAPE, "X mode %d (I=%d) vs Y mode %d (J=%d)", n + 1, x->dims[n], n + 1, y->dims[n]);
+    const int B = x->batch;
+    if (B == 0) return TTC_OK;
+    if (!out_dev) return fail(TTC_ERR_NULL, "out_dev is NULL");
+    if (reinterpret_cast<uintptr_t>(out_dev) & 3u) return fail(TTC_ERR_ALIGN, "out_dev not 4-byte aligned");
+
+    ttc::InnerArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.B = B;
+    a.N = x->order;
+    for (int n = 0; n < a.N; ++n) a.dims[n] = x->dims[n];
+    a.x = to_dev(hx);
+    a.y = to_dev(hy);
+    a.out = out_dev;
+    a.order = nullptr;
+    const int mr = std::max(hx.max_rank, hy.max_rank);
+    a.zmax = mr * mr;
+    a.wbuf = std::max(mr * mr, 8192);
+    const bool uniform = hx.uniform && hy.uniform && hx.urank == hy.urank;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (ttc::inner_fast_supported(a, mr, uniform))
+        e = ttc::launch_inner_fast(a, mr, uniform, s);
+    else
+        e = ttc::launch_inner_generic(a, s);
+    if (e != cudaSuccess) return cuda_fail(e, "ttc_inner launch");
+    return TTC_OK;
+}
+
+ttc_status ttc_pair_cost(const ttc_tt_batch* x, const ttc_tt_batch* y, double* mac, double* bytes) {
+    g_last_error.clear();
+    HostTrain hx, hy;
+    ttc_status st;
+    if ((st = check_batch(x, "X", TTC_MAX_ORDER, &hx)) != TTC_OK) return st;
+    if ((st = check_batch(y, "Y", TTC_MAX_ORDER, &hy)) != TTC_OK) return st;
+    if (x->batch != y->batch || x->order != y->order)
+        return fail(TTC_ERR_SHAPE, "X (B=%d, N=%d) and Y (B=%d, N=%d) differ", x->batch, x->order, y->batch, y->order);
+    for (int n = 0; n < x->order; ++n)
+        if (x->dims[n] != y->dims[n])
+            return fail(TTC_ERR_SHAPE, "X mode %d (I=%d) vs Y mode %d (J=%d)", n + 1, x->dims[n], n + 1, y->dims[n]);
+    for (int b = 0; b < x->batch; ++b) {
+        double m = 0.0, by = 4.0;
+        for (int n = 0; n < x->order; ++n) {
+            const double R = hx.rank(b, n), S = hx.rank(b, n + 1), P = hy.rank(b, n), Q = hy.rank(b, n + 1);
+            const double I = x->dims[n];
+            m += I * std::min(R * P * Q + R * S * Q, R * P * S + P * S * Q);
+            by += 4.0 * I * (R * S + P * Q);
+        }
+        if (mac) mac[b] = m;
+        if (bytes) bytes[b] = by;
+    }
+    return TTC_OK;
+}
+
+// Contiguous k-way split minimising the largest part: binary search on the bottleneck over prefix sums,
+// then greedy fill (each part takes as many pairs as fit under the bottleneck).
+ttc_status ttc_partition(const double* cost, int32_t B, int32_t k, int32_t* bounds) {
+    g_last_error.clear();
+    if (!bounds) return fail(TTC_ERR_NULL, "bounds is NULL");
+    if (B < 0) return fail(TTC_ERR_ARG, "B = %d < 0", B);
+    if (k < 1) return fail(TTC_ERR_ARG, "k = %d < 1", k);
+    if (B > 0 && !cost) return fail(TTC_ERR_NULL, "cost is NULL");
+    double total = 0.0, mx = 0.0;
+    for (int b = 0; b < B; ++b) {
+        if (!(cost[b] >= 0.0)) return fail(TTC_ERR_ARG, "cost[%d] = %g is negative or NaN", b, cost[b]);
+        total += cost[b];
+        mx = std::max(mx, cost[b]);
+    }
+    auto fill = [&](double cap, int32_t* out) -> bool {  // true if B pairs fit in k parts of <= cap
+        int part = 0;
+        double acc = 0.0;
+        if (out) out[0] = 0;
+        for (int b = 0; b < B; ++b) {
+            if (acc + cost[b] > cap && acc > 0.0) {
+                ++part;
+                if (part >= k) return false;
+                if (out) out[part] = b;
+                acc = 0.0;
+            }
+            acc += cost[b];
+        }
+        if (out)
+            for (int j = part + 1; j <= k; ++j) out[j] = B;
+        return true;
+    };
+    if (B == 0 || total == 0.0) {   // equal counts
+        for (int j = 0; j <= k; ++j) bounds[j] = (int32_t)(((int64_t)B * j) / k);
+        return TTC_OK;
+    }
+    double lo = std::max(mx, total / k), hi = total;
+    for (int it = 0; it < 100 && hi - lo > 1e-12 * total; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (fill(mid, nullptr)) hi = mid; else lo = mid;
+    }
+    fill(hi, bounds);
+    // keep every part non-empty when B >= k (bounds strictly increasing)
+    if (B >= k) {
+        for (int j = k - 1; j >= 1; --j) bounds[j] = std::min(bounds[j], bounds[j + 1] - 1);
+        for (int j = 1; j < k; ++j) bounds[j] = std::max(bounds[j], bounds[j - 1] + 1);
+    }
+    return TTC_OK;
+}
+
+}  // extern "C"
+
+// ================================================================================================ contract
+// Host-only plan for the ladder tt_contract (ttc.h; readings R7-R10).
+struct ttc_contract_plan {
+    int B = 0, N = 0, M = 0, K = 0, L = 0;
+    std::vector<int32_t> xdims, ydims, xmodes, ymodes;
+    std::vector<ttc::LadderEl> seq;
+    std::vector<ttc::OutCore> outc;
+    std::vector<int32_t> out_dims, out_src, out_perm;
+    std::vector<int32_t> xranks, yranks;      // host copies [B*(N+1)], [B*(M+1)]
+    std::vector<int32_t> out_ranks;           // [B*(L+1)]
+    std::vector<int64_t> out_offsets;         // [B]
+    int64_t total = 0;
+    int32_t max_rank = 1;
+    bool uniform_out = true;                  // every pair has the same output ranks
+    int64_t scratch_floats = 0;               // per-CTA shared scratch for transfers: TL + TR + 3 tmp
+    int64_t tl_floats = 0, tr_floats = 0, tmp_floats = 0;
+};
+
+namespace {
+
+int64_t core_elems_of(const ttc_contract_plan& p, int b, int l) {
+    const int32_t* r = p.out_ranks.data() + (int64_t)b * (p.L + 1);
+    return (int64_t)r[l] * p.out_dims[l] * r[l + 1];
+}
+
+}  // namespace
+
+extern "C" {
+
+ttc_status ttc_contract_plan_create(const ttc_tt_batch* x, const ttc_tt_batch* y, int32_t npairs,
+                                    const int32_t* x_modes, const int32_t* y_modes, ttc_contract_plan** plan) {
+    g_last_error.clear();
+    if (!plan) return fail(TTC_ERR_NULL, "plan output pointer is NULL");
+    *plan = nullptr;
+    HostTrain hx, hy;
+    ttc_status st;
+    if ((st = check_batch(x, "X", ttc::kMaxContractOrder, &hx)) != TTC_OK) return st;
+    if ((st = check_batch(y, "Y", ttc::kMaxContractOrder, &hy)) != TTC_OK) return st;
+    if (x->batch != y->batch) return fail(TTC_ERR_SHAPE, "batch mismatch: X has %d trains, Y has %d", x->batch, y->batch);
+    const int N = x->order, M = y->order, K = npairs;
+    if (K < 0 || K > std::min(N, M)) return fail(TTC_ERR_MODES, "npairs = %d outside [0, min(N, M) = %d]", K, std::min(N, M));
+    if (K > 0 && (!x_modes || !y_modes)) return fail(TTC_ERR_NULL, "x_modes / y_modes is NULL");
+    for (int k = 0; k < K; ++k) {
+        if (x_modes[k] < 1 || x_modes[k] > N) return fail(TTC_ERR_MODES, "pair %d: X mode %d outside [1, %d]", k + 1, x_modes[k], N);
+        if (y_modes[k] < 1 || y_modes[k] > M) return fail(TTC_ERR_MODES, "pair %d: Y mode %d outside [1, %d]", k + 1, y_modes[k], M);
+        if (k > 0 && (x_modes[k] <= x_modes[k - 1] || y_modes[k] <= y_modes[k - 1]))
+            return fail(TTC_ERR_MODES, "pairs %d, %d: modes must be strictly increasing in both operands "
+                        "(got X %d, %d and Y %d, %d)", k, k + 1, x_modes[k - 1], x_modes[k], y_modes[k - 1], y_modes[k]);
+        if (x->dims[x_modes[k] - 1] != y->dims[y_modes[k] - 1])
+            return fail(TTC_ERR_SHAPE, "X mode %d (I=%d) vs Y mode %d (J=%d)", x_modes[k], x->dims[x_modes[k] - 1],
+                        y_modes[k], y->dims[y_modes[k] - 1]);
+    }
+    std::unique_ptr<ttc_contract_plan> p(new ttc_contract_plan());
+    p->B = x->batch; p->N = N; p->M = M; p->K = K; p->L = N + M - 2 * K;
+    p->xdims.assign(x->dims, x->dims + N);
+    p->ydims.assign(y->dims, y->dims + M);
+    p->xmodes.assign(x_modes, x_modes + K);
+    p->ymodes.assign(y_modes, y_modes + K);
+    // ladder sequence S (R7): per gap k, X free cores, then Y free cores, then transfer T_k
+    for (int k = 1; k <= K + 1; ++k) {
+        const int nprev = k == 1 ? 0 : x_modes[k - 2], mprev = k == 1 ? 0 : y_modes[k - 2];
+        const int ncur = k <= K ? x_modes[k - 1] : N + 1, mcur = k <= K ? y_modes[k - 1] : M + 1;
+        for (int n = nprev + 1; n < ncur; ++n) p->seq.push_back({ttc::EL_XFREE, n - 1, mprev});
+        for (int m = mprev + 1; m < mcur; ++m) p->seq.push_back({ttc::EL_YFREE, m - 1, ncur - 1});
+        if (k <= K) p->seq.push_back({ttc::EL_T, ncur - 1, mcur - 1});
+    }
+    // output cores with their absorbed transfers (R10: into the next core; trailing ones into the last core)
+    int pend_first = -1, pend_count = 0;
+    for (int e = 0; e < (int)p->seq.size(); ++e) {
+        const auto& el = p->seq[e];
+        if (el.kind == ttc::EL_T) {
+            if (pend_count == 0) pend_first = e;
+            ++pend_count;
+            continue;
+        }
+        ttc::OutCore oc{e, pend_count ? pend_first : -1, pend_count, -1, 0};
+        p->outc.push_back(oc);
+        pend_first = -1; pend_count = 0;
+        if (el.kind == ttc::EL_XFREE) { p->out_dims.push_back(x->dims[el.mode]); p->out_src.push_back(el.mode + 1); }
+        else { p->out_dims.push_back(y->dims[el.mode]); p->out_src.push_back(-(el.mode + 1)); }
+    }
+    if (pend_count && !p->outc.empty()) { p->outc.back().rt_first = pend_first; p->outc.back().rt_count = pend_count; }
+    // canonical order (Eq. 8): X free ascending, then Y free ascending -> ladder positions
+    for (int n = 1; n <= N; ++n)
+        for (int l = 0; l < p->L; ++l) if (p->out_src[l] == n) p->out_perm.push_back(l + 1);
+    for (int m = 1; m <= M; ++m)
+        for (int l = 0; l < p->L; ++l) if (p->out_src[l] == -m) p->out_perm.push_back(l + 1);
+    // per-pair ranks, offsets, scratch
+    const int B = p->B, L = p->L;
+    p->xranks.resize((size_t)B * (N + 1));
+    p->yranks.resize((size_t)B * (M + 1));
+    for (int b = 0; b < B; ++b) {
+        for (int n = 0; n <= N; ++n) p->xranks[(size_t)b * (N + 1) + n] = hx.rank(b, n);
+        for (int m = 0; m <= M; ++m) p->yranks[(size_t)b * (M + 1) + m] = hy.rank(b, m);
+    }
+    p->out_ranks.assign((size_t)B * (L + 1), 1);
+    p->out_offsets.assign(B, 0);
+    int64_t off = 0;
+    for (int b = 0; b < B; ++b) {
+        const int32_t* xr = p->xranks.data() + (size_t)b * (N + 1);
+        const int32_t* yr = p->yranks.data() + (size_t)b * (M + 1);
+        int32_t* orr = p->out_ranks.data() + (size_t)b * (L + 1);
+        for (int l = 0; l < L; ++l) {
+            const auto& el = p->seq[p->outc[l].el];
+            int64_t right = el.kind == ttc::EL_XFREE ? (int64_t)xr[el.mode + 1] * yr[el.hold]
+                                                      : (int64_t)xr[el.hold] * yr[el.mode + 1];
+            orr[l + 1] = (int32_t)right;
+        }
+        orr[L] = 1;
+        if (L > 0) orr[0] = 1;
+        int64_t pair_elems = 0;
+        for (int l = 0; l < L; ++l) {
+            int64_t c;
+            if (!mul_ok((int64_t)orr[l] * p->out_dims[l], orr[l + 1], &c) || !add_ok(pair_elems, c, &pair_elems))
+                return fail(TTC_ERR_OVERFLOW, "pair %d: output train size overflows int64", b);
+            p->max_rank = std::max(p->max_rank, orr[l + 1]);
+        }
+        if (L == 0) pair_elems = 1;
+        p->out_offsets[b] = off;
+        if (!add_ok(off, pair_elems, &off)) return fail(TTC_ERR_OVERFLOW, "total output size overflows int64");
+        // scratch: every transfer and chain product of this pair (rows*cols), two temporaries + TL + TR
+        int64_t tmax = 0;
+        for (const auto& el : p->seq)
+            if (el.kind == ttc::EL_T) {
+                const int64_t rows = (int64_t)xr[el.mode] * yr[el.hold], cols = (int64_t)xr[el.mode + 1] * yr[el.hold + 1];
+                tmax = std::max(tmax, rows * cols);
+            }
+        // chain products have the rows of the first transfer and the cols of the current one
+        for (const auto& oc : p->outc)
+            for (int side = 0; side < 2; ++side) {
+                const int f = side ? oc.rt_first : oc.lt_first, c = side ? oc.rt_count : oc.lt_count;
+                if (c <= 0) continue;
+                const auto& e0 = p->seq[f];
+                const int64_t rows = (int64_t)xr[e0.mode] * yr[e0.hold];
+                int64_t cm = 0;
+                for (int t = 0; t < c; ++t) {
+                    const auto& et = p->seq[f + t];
+                    cm = std::max(cm, rows * (int64_t)xr[et.mode + 1] * yr[et.hold + 1]);
+                }
+                int64_t& dst = side ? p->tr_floats : p->tl_floats;
+                dst = std::max(dst, cm);
+                if (c > 1) p->tmp_floats = std::max(p->tmp_floats, std::max(tmax, cm));
+            }
+    }
+    p->total = off;
+    p->scratch_floats = p->tl_floats + p->tr_floats + 3 * p->tmp_floats;
+    const int64_t scratch = p->scratch_floats;
+    for (int b = 1; b < B && p->uniform_out; ++b)
+        for (int l = 0; l <= L; ++l)
+            if (p->out_ranks[(size_t)b * (L + 1) + l] != p->out_ranks[l]) { p->uniform_out = false; break; }
+    if (L > 0 && scratch * (int64_t)sizeof(float) > 200 * 1024)
+        return fail(TTC_ERR_UNSUPPORTED, "transfer scratch of %lld floats exceeds shared memory (ranks too large)",
+                    (long long)scratch);
+    *plan = p.release();
+    return TTC_OK;
+}
+
+ttc_status ttc_contract_plan_query(const ttc_contract_plan* p, int32_t* out_order, int32_t* out_dims, int32_t* out_src,
+                                   int32_t* out_perm, int64_t* total_elems, int32_t* max_rank) {
+    g_last_error.clear();
+    if (!p) return fail(TTC_ERR_NULL, "plan is NULL");
+    if (out_order) *out_order = p->L;
+    if (out_dims) std::copy(p->out_dims.begin(), p->out_dims.end(), out_dims);
+    if (out_src) std::copy(p->out_src.begin(), p->out_src.end(), out_src);
+    if (out_perm) std::copy(p->out_perm.begin(), p->out_perm.end(), out_perm);
+    if (total_elems) *total_elems = p->total;
+    if (max_rank) *max_rank = p->max_rank;
+    return TTC_OK;
+}
+
+ttc_status ttc_contract_plan_layout(const ttc_contract_plan* p, int32_t* out_ranks_host, int64_t* out_offsets_host) {
+    g_last_error.clear();
+    if (!p) return fail(TTC_ERR_NULL, "plan is NULL");
+    if (out_ranks_host) std::copy(p->out_ranks.begin(), p->out_ranks.end(), out_ranks_host);
+    if (out_offsets_host) std::copy(p->out_offsets.begin(), p->out_offsets.end(), out_offsets_host);
+    return TTC_OK;
+}
+
+void ttc_contract_plan_destroy(ttc_contract_plan* p) { delete p; }
+
+ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_cores_dev,
+                        const int64_t* out_offsets_dev, void* stream) {
+    g_last_error.clear();
+    if (!p) return fail(TTC_ERR_NULL, "plan is NULL");
+    HostTrain hx, hy;
+    ttc_status st;
+    if ((st = check_batch(x, "X", ttc::kMaxContractOrder, &hx)) != TTC_OK) return st;
+    if ((st = check_batch(y, "Y", ttc::kMaxContractOrder, &hy)) != TTC_OK) return st;
+    if (x->batch != p->B || y->batch != p->B || x->order != p->N || y->order != p->M)
+        return fail(TTC_ERR_SHAPE, "operands (B=%d/%d, N=%d, M=%d) differ from the plan (B=%d, N=%d, M=%d)", x->batch,
+                    y->batch, x->order, y->order, p->B, p->N, p->M);
+    for (int n = 0; n < p->N; ++n)
+        if (x->dims[n] != p->xdims[n]) return fail(TTC_ERR_SHAPE, "X mode %d: I=%d differs from the plan (%d)", n + 1, x->dims[n], p->xdims[n]);
+    for (int m = 0; m < p->M; ++m)
+        if (y->dims[m] != p->ydims[m]) return fail(TTC_ERR_SHAPE, "Y mode %d: J=%d differs from the plan (%d)", m + 1, y->dims[m], p->ydims[m]);
+    for (int b = 0; b < p->B; ++b) {
+        for (int n = 0; n <= p->N; ++n)
+            if (hx.rank(b, n) != p->xranks[(size_t)b * (p->N + 1) + n])
+                return fail(TTC_ERR_SHAPE, "X pair %d: rank R_%d differs from the plan", b, n);
+        for (int m = 0; m <= p->M; ++m)
+            if (hy.rank(b, m) != p->yranks[(size_t)b * (p->M + 1) + m])
+                return fail(TTC_ERR_SHAPE, "Y pair %d: rank P_%d differs from the plan", b, m);
+    }
+    if (p->B == 0) return TTC_OK;
+    if (!out_cores_dev) return fail(TTC_ERR_NULL, "out_cores_dev is NULL");
+    if (reinterpret_cast<uintptr_t>(out_cores_dev) & 3u) return fail(TTC_ERR_ALIGN, "out_cores_dev not 4-byte aligned");
+    if (!out_offsets_dev && !p->uniform_out)
+        return fail(TTC_ERR_NULL, "pairs have different output ranks: out_offsets_dev is required");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (p->L == 0) {   // every mode contracted: the scalar <X_b, Y_b>, one float per pair (packed)
+        const ttc_status r = ttc_inner(x, y, out_cores_dev, stream);
+        return r;
+    }
+    ttc::ContractArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.B = p->B; a.N = p->N; a.M = p->M; a.K = p->K; a.L = p->L; a.nseq = (int)p->seq.size();
+    for (int n = 0; n < p->N; ++n) a.xdims[n] = p->xdims[n];
+    for (int m = 0; m < p->M; ++m) a.ydims[m] = p->ydims[m];
+    for (int i = 0; i < a.nseq; ++i) a.seq[i] = p->seq[i];
+    for (int l = 0; l < p->L; ++l) a.outc[l] = p->outc[l];
+    a.x = to_dev(hx);
+    a.y = to_dev(hy);
+    a.out = out_cores_dev;
+    a.out_offsets = out_offsets_dev;
+    a.out_pair_elems = p->B ? p->total / p->B : 0;
+    a.tl_off = 0;
+    a.tr_off = (int32_t)p->tl_floats;
+    a.tmp_off = (int32_t)(p->tl_floats + p->tr_floats);
+    a.tmp_size = (int32_t)p->tmp_floats;
+    e = ttc::launch_contract(a, sizeof(float) * (size_t)p->scratch_floats, s);
+    if (e != cudaSuccess) return cuda_fail(e, "ttc_contract launch");
+    return TTC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// ttc_internal.h -- internal (non-ABI) structures shared by the host library and the kernels.
+// Nothing here crosses the C ABI; include/ttc.h is the boundary.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/ttc.h"
+
+namespace ttc {
+
+// One operand batch as the kernels see it.  ranks == nullptr: uniform (1, urank, ..., urank, 1);
+// offsets == nullptr: packed, train b at b * train_elems (uniform ranks only).
+struct TrainDev {
+    const float*   cores;
+    const int32_t* ranks;
+    const int64_t* offsets;
+    int32_t        urank;
+    int64_t        train_elems;
+};
+
+struct InnerArgs {
+    int32_t  B, N;
+    int32_t  dims[TTC_MAX_ORDER];
+    TrainDev x, y;
+    float*   out;
+    const int32_t* order;   // optional device work list (pair indices, e.g. cost-descending); nullptr = identity
+    int32_t  zmax;          // max_n R_n * P_n over the batch (floats)
+    int32_t  wbuf;          // floats of the W chunk buffer (generic kernel)
+};
+
+// Launchers (inner_generic.cu, inner_fast.cu, contract.cu).  Return cudaSuccess or the launch error.
+cudaError_t launch_inner_generic(const InnerArgs& a, cudaStream_t s);
+bool        inner_fast_supported(const InnerArgs& a, int max_rank, bool uniform);
+cudaError_t launch_inner_fast(const InnerArgs& a, int max_rank, bool uniform, cudaStream_t s);
+
+// ---- tt_contract (ladder) ------------------------------------------------------------------------
+enum ElKind : int32_t { EL_XFREE = 1, EL_YFREE = 2, EL_T = 3 };
+
+struct LadderEl {
+    int32_t kind;  // ElKind
+    int32_t mode;  // 0-based: X mode (XFREE, T), Y mode (YFREE)
+    int32_t hold;  // XFREE: Y bond index b carried (P_b); YFREE: X bond index a carried (R_a); T: 0-based Y mode
+};
+
+// One output core of the ladder: the free core it comes from plus the transfers absorbed into it
+// (consecutive transfers multiplied left to right; lt = from the left, rt = from the right).
+struct OutCore {
+    int32_t el;        // index into the ladder sequence of the free core
+    int32_t lt_first;  // first left transfer (index into the sequence), lt_count of them
+    int32_t lt_count;
+    int32_t rt_first;  // trailing transfers absorbed from the right (last core only)
+    int32_t rt_count;
+};
+
+constexpr int kMaxContractOrder = 64;            // N, M <= 64 for ttc_contract (kernel-parameter budget)
+constexpr int kMaxLadder = 2 * kMaxContractOrder + 4;
+
+struct ContractArgs {
+    int32_t  B, N, M, K, L, nseq;
+    int32_t  xdims[kMaxContractOrder];
+    int32_t  ydims[kMaxContractOrder];
+    LadderEl seq[kMaxLadder];
+    OutCore  outc[kMaxLadder];
+    TrainDev x, y;
+    float*   out;
+    const int64_t* out_offsets;   // device [B] or nullptr (uniform: b * out_pair_elems)
+    int64_t  out_pair_elems;
+    int32_t  tl_off, tr_off;      // shared-scratch offsets (floats) of the left / right transfer products
+    int32_t  tmp_off, tmp_size;   // three temporaries of tmp_size floats for chains of >= 2 transfers
+};
+
+cudaError_t launch_contract(const ContractArgs& a, size_t smem_bytes, cudaStream_t s);
+
+}  // namespace ttc

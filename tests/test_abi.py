@@ -1,0 +1,230 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/ttc.h declares, validates
+arguments on the host (every error code), and its host-side plan / cost / partition logic matches the oracle
+and the hand values exactly.  A valid compute call without a GPU must fail (TTC_ERR_CUDA): no CPU fallback."""
+import ctypes
+import itertools
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2109_00626_b200 as ttc
+import ttgen
+from oracle import complexity as cx
+from tests import ref_numpy as ref
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ttc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ttc_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = _declared_symbols()
+    assert len(syms) == 11
+    lib = ctypes.CDLL(ttc.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(ttc.EXPORTED)
+    assert ttc.ttc_version() == 1
+
+
+def _dev(B=2, N=3, dims=(2, 3, 2), R=2, device="cpu"):
+    r = ttgen.uniform_ranks(B, N, R)
+    offs, total = ttgen.packed_offsets(r, dims)
+    return ttc.TTDevice(torch.zeros(total), dims, ranks=r, offsets=offs)
+
+
+def _call_inner(x, y, out=None):
+    out = torch.zeros(max(x.B, 1)) if out is None else out
+    return ttc._lib.ttc_inner(ctypes.byref(x.c), ctypes.byref(y.c), out.data_ptr(), None)
+
+
+def test_valid_inner_without_gpu_is_a_cuda_error_not_a_fallback():
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    x, y = _dev(), _dev()
+    assert _call_inner(x, y) == ttc.TTC_ERR_CUDA
+    assert "ttc_inner launch" in ttc.ttc_last_error()
+
+
+def test_zero_batch_is_a_noop():
+    x, y = _dev(B=0), _dev(B=0)
+    assert ttc._lib.ttc_inner(ctypes.byref(x.c), ctypes.byref(y.c), None, None) == ttc.TTC_OK
+
+
+def test_error_codes():
+    x, y = _dev(), _dev()
+    lib = ttc._lib
+    assert lib.ttc_inner(None, ctypes.byref(y.c), None, None) == ttc.TTC_ERR_NULL
+    # batch mismatch
+    assert _call_inner(x, _dev(B=3)) == ttc.TTC_ERR_SHAPE
+    # mode-size mismatch, diagnostic names both dimensions
+    assert _call_inner(x, _dev(dims=(2, 4, 2))) == ttc.TTC_ERR_SHAPE
+    assert "X mode 2 (I=3) vs Y mode 2 (J=4)" in ttc.ttc_last_error()
+    # boundary rank != 1
+    r = ttgen.uniform_ranks(2, 3, 2)
+    r[1, 3] = 2
+    offs = np.array([0, 100], np.int64)
+    bad = ttc.TTDevice(torch.zeros(300), (2, 3, 2), ranks=r, offsets=offs)
+    assert _call_inner(bad, y) == ttc.TTC_ERR_RANK
+    assert "pair 1" in ttc.ttc_last_error()
+    r2 = ttgen.uniform_ranks(2, 3, 2)
+    r2[0, 1] = 0
+    assert _call_inner(ttc.TTDevice(torch.zeros(300), (2, 3, 2), ranks=r2, offsets=offs), y) == ttc.TTC_ERR_RANK
+    # rank above the supported maximum
+    big = ttc.TTDevice(torch.zeros(10), (2, 3, 2), uniform_rank=129, batch=2)
+    assert _call_inner(big, y) == ttc.TTC_ERR_UNSUPPORTED
+    # trains past the end of the buffer
+    short = ttc.TTDevice(torch.zeros(5), (2, 3, 2), uniform_rank=2, batch=2)
+    assert _call_inner(short, y) == ttc.TTC_ERR_OVERFLOW
+    # misaligned output
+    buf = torch.zeros(8)
+    assert lib.ttc_inner(ctypes.byref(x.c), ctypes.byref(y.c), buf.data_ptr() + 2, None) == ttc.TTC_ERR_ALIGN
+    # misaligned cores
+    xm = _dev()
+    xm.c.cores = xm.cores.data_ptr() + 1
+    assert _call_inner(xm, y) == ttc.TTC_ERR_ALIGN
+    # negative batch / order
+    xn = _dev()
+    xn.c.batch = -1
+    assert _call_inner(xn, y) == ttc.TTC_ERR_ARG
+    xo = _dev()
+    xo.c.order = 0
+    assert _call_inner(xo, y) == ttc.TTC_ERR_SHAPE
+    # offset overflow
+    r3 = ttgen.uniform_ranks(2, 3, 2)
+    r3[0, 1] = 3
+    ov = ttc.TTDevice(torch.zeros(300), (2, 3, 2), ranks=r3, offsets=np.array([0, 2 ** 62], np.int64))
+    assert _call_inner(ov, y) == ttc.TTC_ERR_OVERFLOW
+    with pytest.raises(ttc.TTCError):
+        ttc.ttc_inner(x, _dev(B=3), out=torch.zeros(2))
+
+
+def test_contract_mode_errors():
+    x, y = _dev(), _dev()
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_contract_plan_create(x, y, [1, 3], [3, 1])
+    assert e.value.status == ttc.TTC_ERR_MODES
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_contract_plan_create(x, y, [4], [1])
+    assert e.value.status == ttc.TTC_ERR_MODES
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_contract_plan_create(x, y, [1], [2])        # I_1 = 2 vs J_2 = 3
+    assert e.value.status == ttc.TTC_ERR_SHAPE
+    assert "X mode 1 (I=2) vs Y mode 2 (J=3)" in ttc.ttc_last_error()
+
+
+def _monotone(N, M, K):
+    for xm in itertools.combinations(range(1, N + 1), K):
+        for ym in itertools.combinations(range(1, M + 1), K):
+            yield list(xm), list(ym)
+
+
+def test_contract_plan_metadata_matches_oracle_exhaustive():
+    """Host plan (ladder order, dims, src, perm, per-pair ranks and sizes) == oracle O3, exactly."""
+    rng = np.random.default_rng(0)
+    n = 0
+    for N, M in [(1, 1), (2, 3), (3, 3), (4, 2), (3, 5)]:
+        for K in range(0, min(N, M) + 1):
+            for xm, ym in _monotone(N, M, K):
+                xd = list(rng.integers(1, 4, N))
+                yd = list(rng.integers(1, 4, M))
+                for a, b in zip(xm, ym):
+                    yd[b - 1] = xd[a - 1]
+                B = 3
+                xr = np.stack([[1] + list(rng.integers(1, 5, N - 1)) + [1] for _ in range(B)]).astype(np.int32)
+                yr = np.stack([[1] + list(rng.integers(1, 5, M - 1)) + [1] for _ in range(B)]).astype(np.int32)
+                xo, xt = ttgen.packed_offsets(xr, xd)
+                yo, yt = ttgen.packed_offsets(yr, yd)
+                X = ttc.TTDevice(torch.zeros(xt), xd, ranks=xr, offsets=xo)
+                Y = ttc.TTDevice(torch.zeros(yt), yd, ranks=yr, offsets=yo)
+                plan = ttc.ttc_contract_plan_create(X, Y, xm, ym)
+                total = 0
+                for b in range(B):
+                    Xc = ref.random_train(rng, xd, xr[b])
+                    Yc = ref.random_train(rng, yd, yr[b])
+                    res = oracle.tt_contract(Xc, Yc, xm, ym, with_cores=False)
+                    assert plan.L == res["order"]
+                    assert list(plan.dims) == list(res["dims"])
+                    assert list(plan.src) == list(res["src"])
+                    assert list(plan.perm) == list(res["perm"])
+                    assert list(plan.ranks[b]) == list(res["ranks"])
+                    assert plan.offsets[b] == total
+                    total += res["elems"]
+                assert plan.total == total
+                n += 1
+    assert n > 50
+
+
+def test_c3_plan_hand_values():
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "c3_ladder_meta.json")))
+    X = ttc.TTDevice(torch.zeros(1), [8] * 6, uniform_rank=8, batch=0)
+    Y = ttc.TTDevice(torch.zeros(1), [8] * 6, uniform_rank=8, batch=0)
+    x1 = ttc.TTDevice(torch.zeros(2 * 8 * 8 + 4 * 8 * 64), [8] * 6, uniform_rank=8, batch=1)
+    plan = ttc.ttc_contract_plan_create(x1, x1, g["x_modes"], g["y_modes"])
+    assert plan.L == g["order"] and list(plan.dims) == g["dims"] and list(plan.src) == g["src"]
+    assert list(plan.perm) == g["perm"] and list(plan.ranks[0]) == g["ranks"] and plan.total == g["elems"]
+    assert plan.max_rank == 64
+
+
+def test_pair_cost_matches_closed_forms():
+    for cfg, mac_want, bytes_want in (("C1", 4240, 4480), ("C2", 795136, 200704), ("C4", 29393408, 1839104)):
+        c = ttgen.CONFIGS[cfg]
+        x = ttc.TTDevice(torch.zeros(1), [c["I"]] * c["N"], uniform_rank=c["R"], batch=0)
+        r = ttgen.uniform_ranks(2, c["N"], c["R"])
+        offs, tot = ttgen.packed_offsets(r, [c["I"]] * c["N"])
+        X = ttc.TTDevice(torch.zeros(tot), [c["I"]] * c["N"], ranks=r, offsets=offs)
+        mac, by = ttc.ttc_pair_cost(X, X)
+        assert list(mac) == [mac_want] * 2
+        assert list(by) == [bytes_want + 4] * 2   # cores read once + the 4-byte result
+    # heterogeneous (C5 shape): min-association cost, checked against the W-first oracle count as an upper bound
+    X, Y = ttgen.config_batch("C5", B=4)
+    XD, YD = ttc.TTDevice.from_batch(X), ttc.TTDevice.from_batch(Y)
+    mac, by = ttc.ttc_pair_cost(XD, YD)
+    for b in range(4):
+        dims = list(X.dims)
+        w_first = cx.sweep_macs(dims, list(X.ranks[b]), list(Y.ranks[b]))
+        v_first = cx.sweep_macs(dims, list(Y.ranks[b]), list(X.ranks[b]))
+        assert mac[b] <= min(w_first, v_first)
+        per_step = sum(dims[n] * min(X.ranks[b, n] * Y.ranks[b, n] * Y.ranks[b, n + 1] + X.ranks[b, n] * X.ranks[b, n + 1] * Y.ranks[b, n + 1],
+                                     X.ranks[b, n] * Y.ranks[b, n] * X.ranks[b, n + 1] + Y.ranks[b, n] * X.ranks[b, n + 1] * Y.ranks[b, n + 1])
+                       for n in range(len(dims)))
+        assert mac[b] == per_step
+        assert by[b] == 4 * (sum(X.ranks[b, n] * dims[n] * X.ranks[b, n + 1] + Y.ranks[b, n] * dims[n] * Y.ranks[b, n + 1]
+                                 for n in range(len(dims))) + 1)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_partition_is_optimal_contiguous_split(seed):
+    """Bottleneck of ttc_partition == brute-force optimum over all contiguous k-splits (small B)."""
+    rng = np.random.default_rng(seed)
+    B = int(rng.integers(1, 11))
+    k = int(rng.integers(1, 5))
+    cost = rng.uniform(0.5, 3.0, B)
+    bounds = ttc.ttc_partition(cost, k)
+    assert bounds[0] == 0 and bounds[-1] == B and np.all(np.diff(bounds) >= 0)
+    if B >= k:
+        assert np.all(np.diff(bounds) >= 1)
+    got = max(cost[bounds[j]:bounds[j + 1]].sum() for j in range(k))
+    best = np.inf
+    for cuts in itertools.combinations(range(1, B), min(k - 1, B - 1)):
+        bb = [0, *cuts, B]
+        best = min(best, max(cost[bb[j]:bb[j + 1]].sum() for j in range(len(bb) - 1)))
+    assert got <= best * (1 + 1e-9)
+
+
+def test_partition_uniform_and_errors():
+    b = ttc.ttc_partition(np.ones(4096), 8)
+    assert list(b) == [512 * j for j in range(9)]
+    with pytest.raises(ttc.TTCError):
+        ttc.ttc_partition(np.ones(4), 0)
+    with pytest.raises(ttc.TTCError):
+        ttc.ttc_partition(np.array([1.0, -1.0]), 2)

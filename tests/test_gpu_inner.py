@@ -1,0 +1,180 @@
+"""GPU parity for ttc_inner (through the C ABI) against the fp64 oracle, on the BASELINE.json configs.
+
+Error measure (BASELINE.json north_star): |gpu - oracle| / (||X||_F ||Y||_F) <= 1e-4, with the norms from
+the oracle.  Because that bound is nearly vacuous for iid pairs (|<X,Y>| / (||X|| ||Y||) ~ 1e-5 .. 1e-10,
+DESIGN.md reading R12), parity is gated on non-vacuous batches of the same shapes: self pairs (Y = X),
+correlated pairs, integer cores (bitwise exact) and tagged rank-1 pairs (bitwise exact, order check); on
+iid batches the error must also be far below |oracle| itself."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2109_00626_b200 as ttc
+import ttgen
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+TOL = 1e-4
+
+
+def _run(X, Y):
+    out = ttc.ttc_inner(ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV))
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+def _check(X, Y, got, idx, kind):
+    worst = 0.0
+    for b in idx:
+        xc, yc = X.train(b), Y.train(b)
+        want, _ = oracle.tt_inner(xc, yc)
+        nrm = oracle.normaliser(xc, yc)
+        err = abs(got[b] - want) / nrm
+        worst = max(worst, err)
+        assert err <= TOL, f"{kind} pair {b}: normalised error {err:.3e}"
+        if kind in ("self", "corr"):
+            assert abs(want) / nrm > 0.5            # the control is not vacuous here
+            assert abs(got[b] - want) <= 1e-5 * abs(want)
+        if kind == "iid" and abs(want) / nrm > 1e-7:
+            assert abs(got[b] - want) <= 1e-2 * abs(want), f"iid pair {b}: {got[b]} vs {want}"
+    return worst
+
+
+def _sample(B, k, seed=0):
+    if B <= k:
+        return list(range(B))
+    rng = np.random.default_rng(seed)
+    return sorted(set([0, B - 1] + list(rng.choice(B, k - 2, replace=False))))
+
+
+@pytest.mark.parametrize("kind", ["iid", "self", "corr"])
+def test_c1(kind):
+    X, Y = ttgen.config_batch("C1", kind=kind)
+    got = _run(X, Y)
+    _check(X, Y, got, [0], kind)
+
+
+@pytest.mark.parametrize("kind", ["iid", "self", "corr"])
+def test_c2_small_all_pairs(kind):
+    """C2 shape, 67 pairs (several waves' worth of CTAs per SM is not needed here: a ragged batch)."""
+    X, Y = ttgen.config_batch("C2", kind=kind, B=67)
+    got = _run(X, Y)
+    _check(X, Y, got, range(67), kind)
+
+
+def test_c2_full_size_sampled():
+    """BASELINE.json configs[1] at full size (4096 pairs, the bench workload), sampled pairs vs the oracle."""
+    X, Y = ttgen.config_batch("C2", kind="iid", device=DEV)
+    got = _run(X, Y)
+    _check(X, Y, got, _sample(X.B, 24), "iid")
+    Xs, Ys = ttgen.config_batch("C2", kind="self", device=DEV)
+    got = _run(Xs, Ys)
+    _check(Xs, Ys, got, _sample(Xs.B, 16, 1), "self")
+
+
+def test_c4_sampled():
+    """BASELINE.json configs[3] (R=64): 512 pairs, sampled."""
+    for kind in ("iid", "self"):
+        X, Y = ttgen.config_batch("C4", kind=kind, B=512, device=DEV)
+        got = _run(X, Y)
+        _check(X, Y, got, _sample(X.B, 8), kind)
+
+
+def test_c5_sampled():
+    """BASELINE.json configs[4] (heterogeneous ranks {8..32}, N=64, I=2): one 8-GPU shard (8192 pairs)."""
+    X, Y = ttgen.config_batch("C5", kind="iid", B=8192, device=DEV)
+    got = _run(X, Y)
+    _check(X, Y, got, _sample(X.B, 16), "iid")
+    X, Y = ttgen.config_batch("C5", kind="corr", B=256, device=DEV)
+    got = _run(X, Y)
+    _check(X, Y, got, _sample(X.B, 16, 2), "corr")
+
+
+@pytest.mark.parametrize("cfg,B", [("C1", 1), ("C2", 33), ("C4", 8), ("C5", 16)])
+def test_integer_cores_bitwise(cfg, B):
+    """Cores in {-1, 0, 1}: when every partial sum is an integer below 2^24 (checked by running the oracle on
+    |X|, |Y|, an upper bound for any summation order), fp32 is exact and the GPU must equal the oracle bitwise."""
+    c = ttgen.CONFIGS[cfg]
+    if cfg == "C5":
+        xr = ttgen.random_ranks(1, 5, 0, 0, B, c["N"], c["rank_choices"])
+        yr = ttgen.random_ranks(1, 5, 1, 0, B, c["N"], c["rank_choices"])
+        dims = (c["I"],) * c["N"]
+    else:
+        xr = yr = ttgen.uniform_ranks(B, c["N"], c["R"])
+        dims = (c["I"],) * c["N"]
+    density = {"C1": 0.3, "C2": 0.05, "C4": 0.01, "C5": 0.1}[cfg]
+    X, Y = ttgen.make_pair("int", 3, 9, 0, xr, dims, yr, density=density)
+    got = _run(X, Y)
+    exact = 0
+    for b in range(B):
+        xc, yc = X.train(b), Y.train(b)
+        bound, _ = oracle.tt_inner([np.abs(a) for a in xc], [np.abs(a) for a in yc])
+        if bound >= 2 ** 24:
+            continue
+        want, _ = oracle.tt_inner(xc, yc)
+        assert got[b] == want, f"pair {b}: {got[b]} != {want}"
+        exact += 1
+    assert exact >= 1
+
+
+def test_tagged_order():
+    """<X_b, Y_b> = b exactly: results come back in pair order (C2 shape, 1000 pairs)."""
+    B = 1000
+    X, Y = ttgen.make_pair("tagged", 0, 2, 0, ttgen.uniform_ranks(B, 8, 16), (16,) * 8)
+    got = _run(X, Y)
+    assert np.array_equal(got, np.arange(B, dtype=np.float64))
+
+
+def test_determinism_and_exact_scaling():
+    X, Y = ttgen.config_batch("C2", kind="iid", B=64)
+    a, b = _run(X, Y), _run(X, Y)
+    assert np.array_equal(a, b)
+    # scaling core 3 of every X by 2 scales every result by exactly 2
+    X2 = ttgen.TTBatch(X.cores.clone(), X.ranks, X.offsets, X.dims)
+    sz = [16 * 16 * 16] * 6
+    start = 256 + sz[0] * 2  # core index 3 (0-based) starts after cores 0 (256), 1, 2
+    per = int(X.offsets[1])
+    for j in range(64):
+        X2.cores[j * per + start: j * per + start + 4096] *= 2
+    c = _run(X2, Y)
+    assert np.array_equal(c, 2 * a)
+
+
+def test_virtual_shards_are_bitwise_equal():
+    """Sharding the batch (ttc_partition) and running the shards one after the other gives bitwise the
+    unsharded result: per-pair work is independent of the split (multi-GPU correctness)."""
+    X, Y = ttgen.config_batch("C5", kind="iid", B=200)
+    XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+    full = ttc.ttc_inner(XD, YD).cpu().numpy()
+    mac, _ = ttc.ttc_pair_cost(XD, YD)
+    for k in (2, 4, 8):
+        bounds = ttc.ttc_partition(mac, k)
+        parts = []
+        for j in range(k):
+            s, e = int(bounds[j]), int(bounds[j + 1])
+            xs = ttc.TTDevice(X.cores.to(DEV), X.dims, ranks=X.ranks[s:e], offsets=X.offsets[s:e])
+            ys = ttc.TTDevice(Y.cores.to(DEV), Y.dims, ranks=Y.ranks[s:e], offsets=Y.offsets[s:e])
+            parts.append(ttc.ttc_inner(xs, ys).cpu().numpy())
+        assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_edge_shapes():
+    """N = 1 (a dot product), I = 1 modes, rank-1 trains, unequal X / Y ranks, odd sizes, large I."""
+    rng = np.random.default_rng(5)
+    for dims, rx, ry in [((7,), [1, 1], [1, 1]),
+                         ((1, 1, 1), [1, 3, 2, 1], [1, 1, 5, 1]),
+                         ((3, 1, 4, 2), [1, 5, 7, 3, 1], [1, 2, 9, 4, 1]),
+                         ((300, 2), [1, 3, 1], [1, 5, 1]),
+                         ((5, 5, 5), [1, 128, 128, 1], [1, 128, 128, 1]),
+                         ((2,) * 10, [1] + [33] * 9 + [1], [1] + [31] * 9 + [1])]:
+        B = 5
+        xr = np.tile(np.array(rx, np.int32), (B, 1))
+        yr = np.tile(np.array(ry, np.int32), (B, 1))
+        X = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, xr, dims, "geo")
+        Y = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 1, 0, yr, dims, "geo")
+        got = _run(X, Y)
+        _check(X, Y, got, range(B), "edge")
+        Xs = ttgen.TTBatch(X.cores.clone(), X.ranks, X.offsets, X.dims)
+        got = _run(Xs, Xs)
+        _check(Xs, Xs, got, range(B), "self")
