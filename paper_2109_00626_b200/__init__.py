@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libttc.so")
+LIB_PATH = os.environ.get("TTC_LIB_PATH") or os.path.join(_HERE, "libttc.so")   # override: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -196,7 +197,20 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     const bool uniform = hx.uniform && hy.uniform && hx.urank == hy.urank;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    if (ttc::inner_fast_supported(a, mr, uniform))
+    // TTC_KERNEL=generic|fast forces the general-shape / the ranks<=32 kernel (variant cross-checks in tests/)
+    const char* kv = std::getenv("TTC_KERNEL");
+    const bool force_generic = kv && std::strcmp(kv, "generic") == 0;
+    // uniform rank-16 trains with 16-byte aligned cores and trains: the specialised rank-16 kernel
+    bool aligned16 = ((reinterpret_cast<uintptr_t>(x->cores) | reinterpret_cast<uintptr_t>(y->cores)) & 15u) == 0;
+    for (int b = 0; aligned16 && b < B; ++b) {
+        if (x->offsets_host && (x->offsets_host[b] & 3)) aligned16 = false;
+        if (y->offsets_host && (y->offsets_host[b] & 3)) aligned16 = false;
+    }
+    const bool uniform_r16 = uniform && hx.urank == 16 && aligned16 && (hx.train_elems_uniform & 3) == 0;
+    const bool force_fast = kv && std::strcmp(kv, "fast") == 0;
+    if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
+        e = ttc::launch_inner_r16(a, s);
+    else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);
     else
         e = ttc::launch_inner_generic(a, s);

@@ -178,3 +178,16 @@ def test_edge_shapes():
         Xs = ttgen.TTBatch(X.cores.clone(), X.ranks, X.offsets, X.dims)
         got = _run(Xs, Xs)
         _check(Xs, Xs, got, range(B), "self")
+
+
+def test_kernel_variants_agree(monkeypatch):
+    """The specialised kernel and the general-shape kernel (TTC_KERNEL=generic) agree within fp32 rounding."""
+    for cfg, B in (("C2", 16), ("C5", 8), ("C1", 1)):
+        X, Y = ttgen.config_batch(cfg, kind="corr", B=B)
+        fast = _run(X, Y)
+        monkeypatch.setenv("TTC_KERNEL", "generic")
+        gen = _run(X, Y)
+        monkeypatch.delenv("TTC_KERNEL")
+        for b in range(B):
+            nrm = oracle.normaliser(X.train(b), Y.train(b))
+            assert abs(fast[b] - gen[b]) <= 1e-5 * nrm

@@ -49,6 +49,20 @@ __global__ void mma_bf16_kernel(float* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// latency: one warp, one dependent chain of mma.sync
+__global__ void mma_lat_kernel(float* out, int iters, long long* cycles) {
+    uint32_t a0 = threadIdx.x, a1 = a0 ^ 1, a2 = a0 ^ 2, a3 = a0 ^ 3, b0 = a0 ^ 5, b1 = a0 ^ 7;
+    float d[4] = {};
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i)
+        asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                     : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                     : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    long long t1 = clock64();
+    if (threadIdx.x == 0) *cycles = t1 - t0;
+    out[threadIdx.x] = d[0] + d[1] + d[2] + d[3];
+}
+
 __global__ void read_kernel(const float4* __restrict__ in, size_t n, float* out) {
     float acc = 0;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -103,6 +117,14 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         double fl = 2.0 * 16 * 8 * 16 * (blocks * threads / 32.0) * iters * 4;
         printf(", \"mma_sync_bf16_tflops\": %.2f", fl / ms / 1e9);
+    }
+    {
+        long long* cyc;
+        CK(cudaMalloc(&cyc, 8));
+        mma_lat_kernel<<<1, 32>>>(out, 1000, cyc);
+        long long c = 0;
+        CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
+        printf(", \"mma_sync_tf32_latency_cycles\": %.1f", c / 1000.0);
     }
     {
         size_t bytes = (size_t)4 << 30;

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "inner" > gpurun_out/pytest_gpu10.log 2>&1
+for c in C2 C5; do timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench10_${c}.json 2> gpurun_out/bench10_${c}.err; done
+TTC_LIB_PATH=$PWD/build/alt/libttc_112.so timeout 300 python bench.py --config C2 --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench10_C2_112.json 2> gpurun_out/bench10_C2_112.err
+CMD="python bench.py --config C2 --steps 2 --warmup 1 --no-cpu --no-e2e"
+$CMD > gpurun_out/plain10.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:inner_tc -s 1 -c 1 -o gpurun_out/prof10_c2 $CMD > gpurun_out/ncu10.log 2>&1
+echo done
