@@ -14,11 +14,25 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Division by a runtime constant d >= 1 for 0 <= n < 2^31 without the integer-divide sequence
+// (Granlund-Montgomery): q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = 2^32 (2^l - d) / d + 1.
+struct FastDiv {
+    uint32_t d, m, l;
+    __device__ __forceinline__ void init(uint32_t dd) {
+        d = dd;
+        l = 0;
+        while ((1u << l) < d) ++l;
+        m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << l) - d)) / d + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> l; }
+};
+
 struct PairCtx {
     int32_t rx[kMaxContractOrder + 1], ry[kMaxContractOrder + 1];
     int64_t xo[kMaxContractOrder + 1], yo[kMaxContractOrder + 1];   // core offsets within the train
     int32_t orr[kMaxLadder + 1];                                     // output bond ranks
     int64_t oo[kMaxLadder + 1];                                      // output core offsets within the pair
+    FastDiv fd[4];   // divisors of the core being emitted: quads per column, I, right-bond split, H
 };
 
 __device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, float d) {
@@ -36,12 +50,38 @@ __device__ void build_transfer(const ContractArgs& a, const PairCtx& c, const fl
     const float* X = xc + c.xo[n];
     const float* Y = yc + c.yo[m];
     const int rows = R * P, total = rows * Rn * Pn;
+    if ((R & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15u) == 0) && ((I * R) & 3) == 0) {
+        // four consecutive r per thread: X[r..r+3, i, r'] is one 16-byte load
+        const int R4 = R >> 2, total4 = total >> 2;
+        for (int e = threadIdx.x; e < total4; e += blockDim.x) {
+            int q = e;
+            const int r4 = q % R4; q /= R4;
+            const int p = q % P; q /= P;
+            const int rr = q % Rn, pp = q / Rn;
+            const float* xp = X + 4 * r4 + R * I * rr;
+            const float* yp = Y + p + P * I * pp;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = 0; i < I; ++i) {
+                const float4 xv = *reinterpret_cast<const float4*>(xp + R * i);
+                const float yv = yp[P * i];
+                acc.x = fmaf(xv.x, yv, acc.x); acc.y = fmaf(xv.y, yv, acc.y);
+                acc.z = fmaf(xv.z, yv, acc.z); acc.w = fmaf(xv.w, yv, acc.w);
+            }
+            float* d = dst + 4 * r4 + R * (p + P * (rr + Rn * pp));
+            d[0] = acc.x; d[1] = acc.y; d[2] = acc.z; d[3] = acc.w;
+        }
+        return;
+    }
+    // (r, p, r', p') of entry e by nested loops: e = r + R (p + P (r' + R' p'))
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int row = e % rows, col = e / rows;
-        const int r = row % R, p = row / R, rr = col % Rn, pp = col / Rn;
+        int q = e;
+        const int r = q % R; q /= R;
+        const int p = q % P; q /= P;
+        const int rr = q % Rn, pp = q / Rn;
+        const float* xp = X + r + R * I * rr;
+        const float* yp = Y + p + P * I * pp;
         float acc = 0.0f;
-        for (int i = 0; i < I; ++i)
-            acc = fmaf(__ldg(X + r + R * (i + I * rr)), __ldg(Y + p + P * (i + I * pp)), acc);
+        for (int i = 0; i < I; ++i) acc = fmaf(xp[R * i], yp[P * i], acc);
         dst[e] = acc;
     }
 }
@@ -105,23 +145,23 @@ __device__ __forceinline__ float cprime(const FreeCore& f, const float* TL, int 
         const float* col = f.G + f.Rb * (i + f.I * rr);
         if (has_tl) {
             float acc = 0.0f;
-            for (int r = 0; r < f.Rb; ++r) acc = fmaf(TL[alpha + Aout * (r + f.Rb * pp)], __ldg(col + r), acc);
+            for (int r = 0; r < f.Rb; ++r) acc = fmaf(TL[alpha + Aout * (r + f.Rb * pp)], col[r], acc);
             return acc;
         }
         const int r = alpha - f.Rb * pp;
-        return (r >= 0 && r < f.Rb) ? __ldg(col + r) : 0.0f;
+        return (r >= 0 && r < f.Rb) ? col[r] : 0.0f;
     } else {         // [r + H p, j, r' + H p'] = delta_{r r'} Y[p, j, p']
         const int rr = gamma % f.H, pp = gamma / f.H;
         const float* col = f.G + f.Rb * (i + f.I * pp);
         if (has_tl) {
             float acc = 0.0f;
-            for (int p = 0; p < f.Rb; ++p) acc = fmaf(TL[alpha + Aout * (rr + f.H * p)], __ldg(col + p), acc);
+            for (int p = 0; p < f.Rb; ++p) acc = fmaf(TL[alpha + Aout * (rr + f.H * p)], col[p], acc);
             return acc;
         }
         const int d = alpha - rr;
         if (d < 0 || d % f.H) return 0.0f;
         const int p = d / f.H;
-        return p < f.Rb ? __ldg(col + p) : 0.0f;
+        return p < f.Rb ? col[p] : 0.0f;
     }
 }
 
@@ -145,59 +185,123 @@ __device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* 
     const int I = f.I;
     const int64_t total = (int64_t)Aout * I * Bout;
     float* dst = out + c.oo[l];
-    const bool quad_ok = (Aout % 4 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+    const bool quad_ok = (Aout % 4 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) && total < (1ll << 31);
     if (!has_tr && quad_ok) {
-        // 4 consecutive alpha of one column per thread -> one 16-byte streaming store
+        // 4 consecutive alpha of one column per thread -> one 16-byte streaming store; consecutive threads write
+        // consecutive quads (coalesced).  Column / row decompositions by precomputed magic-number division.
         const int qpc = Aout / 4;
-        const int64_t nq = total / 4;
-        for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
-            const int col = (int)(q / qpc);
-            const int a0 = (int)(q - (int64_t)col * qpc) * 4;
-            const int i = col % I, beta = col / I;
+        const FastDiv dq = c.fd[0], di = c.fd[1], db = c.fd[2], dh = c.fd[3];
+        const uint32_t nq = (uint32_t)(total / 4);
+        const int Bsplit = f.xfree ? f.Rn : f.H;   // beta = rr + Bsplit * pp
+        // When blockDim is a multiple of qpc each thread keeps one alpha-quad a0 and walks the columns
+        // col = i + I * (rr + Bsplit * pp) in steps of blockDim / qpc: (i, rr, pp) are updated incrementally,
+        // no division inside the loop.  Otherwise every quad is decomposed by magic-number division.
+        const bool walk = (blockDim.x % qpc) == 0;
+        const uint32_t cstep = blockDim.x / qpc;                 // columns advanced per iteration (walk)
+        const int step_i = (int)(cstep % (uint32_t)I), step_b = (int)(cstep / (uint32_t)I);
+        const int step_rr = step_b % Bsplit, step_pp = step_b / Bsplit;
+        int a0 = 0, i = 0, rr = 0, pp = 0;
+        {
+            const uint32_t q0 = threadIdx.x;
+            const uint32_t col = dq.div(q0);
+            a0 = (int)(q0 - col * qpc) * 4;
+            const uint32_t beta = di.div(col);
+            i = (int)(col - beta * I);
+            const uint32_t pq = db.div(beta);
+            pp = (int)pq;
+            rr = (int)(beta - pq * Bsplit);
+        }
+        const int d_pb = (int)dh.div((uint32_t)a0);   // walk: this thread's alpha-quad block (fixed)
+        for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+            if (!walk) {
+                const uint32_t col = dq.div(q);
+                a0 = (int)(q - col * qpc) * 4;
+                const uint32_t beta = di.div(col);
+                i = (int)(col - beta * I);
+                const uint32_t pq = db.div(beta);
+                pp = (int)pq;
+                rr = (int)(beta - pq * Bsplit);
+            }
             float v[4];
-            if (f.xfree) {
-                const int rr = beta % f.Rn, pp = beta / f.Rn;
+            if (f.xfree) {   // [r + R p, i, r' + R' p'] = X[r, i, r'] delta_{p p'}
                 const float* gcol = f.G + f.Rb * (i + I * rr);
-                if (has_tl) {
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (has_tl) {   // two accumulators (even / odd r): half the dependent-FMA chain
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), ac2 = acc;
                     const float* tl = TL + a0 + Aout * (f.Rb * pp);
-                    for (int r = 0; r < f.Rb; ++r) {
-                        const float g = __ldg(gcol + r);
+                    int r = 0;
+                    for (; r + 1 < f.Rb; r += 2) {
+                        const float g = gcol[r], g2 = gcol[r + 1];
+                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * r);
+                        const float4 t2 = *reinterpret_cast<const float4*>(tl + Aout * (r + 1));
+                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
+                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
+                        ac2.x = fmaf(t2.x, g2, ac2.x); ac2.y = fmaf(t2.y, g2, ac2.y);
+                        ac2.z = fmaf(t2.z, g2, ac2.z); ac2.w = fmaf(t2.w, g2, ac2.w);
+                    }
+                    if (r < f.Rb) {
+                        const float g = gcol[r];
                         const float4 t = *reinterpret_cast<const float4*>(tl + Aout * r);
                         acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
                         acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
                     }
-                    v[0] = acc.x; v[1] = acc.y; v[2] = acc.z; v[3] = acc.w;
+                    v[0] = acc.x + ac2.x; v[1] = acc.y + ac2.y; v[2] = acc.z + ac2.z; v[3] = acc.w + ac2.w;
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int r = a0 + k - f.Rb * pp;
-                        v[k] = (r >= 0 && r < f.Rb) ? __ldg(gcol + r) : 0.0f;
+                        v[k] = (r >= 0 && r < f.Rb) ? gcol[r] : 0.0f;
                     }
                 }
-            } else {
-                const int rr = beta % f.H, pp = beta / f.H;
+            } else {         // [r + H p, j, r' + H p'] = delta_{r r'} Y[p, j, p']
                 const float* gcol = f.G + f.Rb * (i + I * pp);
-                if (has_tl) {
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (has_tl) {   // two accumulators (even / odd p)
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), ac2 = acc;
                     const float* tl = TL + a0 + Aout * rr;
-                    for (int p = 0; p < f.Rb; ++p) {
-                        const float g = __ldg(gcol + p);
+                    int p = 0;
+                    for (; p + 1 < f.Rb; p += 2) {
+                        const float g = gcol[p], g2 = gcol[p + 1];
+                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * f.H * p);
+                        const float4 t2 = *reinterpret_cast<const float4*>(tl + Aout * f.H * (p + 1));
+                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
+                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
+                        ac2.x = fmaf(t2.x, g2, ac2.x); ac2.y = fmaf(t2.y, g2, ac2.y);
+                        ac2.z = fmaf(t2.z, g2, ac2.z); ac2.w = fmaf(t2.w, g2, ac2.w);
+                    }
+                    if (p < f.Rb) {
+                        const float g = gcol[p];
                         const float4 t = *reinterpret_cast<const float4*>(tl + Aout * f.H * p);
                         acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
                         acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
                     }
-                    v[0] = acc.x; v[1] = acc.y; v[2] = acc.z; v[3] = acc.w;
+                    v[0] = acc.x + ac2.x; v[1] = acc.y + ac2.y; v[2] = acc.z + ac2.z; v[3] = acc.w + ac2.w;
+                } else if (f.H >= 4) {
+                    // alpha = r + H p is nonzero only for r = r': within 4 consecutive alpha at most one hit
+                    const int pb = walk ? d_pb : (int)dh.div((uint32_t)a0);
+                    const int k = rr - (a0 - pb * f.H);   // position of alpha = r' + H pb inside the quad
+                    const float val = ((unsigned)k < 4u && pb < f.Rb) ? gcol[pb] : 0.0f;
+                    v[0] = k == 0 ? val : 0.0f;
+                    v[1] = k == 1 ? val : 0.0f;
+                    v[2] = k == 2 ? val : 0.0f;
+                    v[3] = k == 3 ? val : 0.0f;
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int d = a0 + k - rr;
-                        const int p = d / f.H;
-                        v[k] = (d >= 0 && d - p * f.H == 0 && p < f.Rb) ? __ldg(gcol + p) : 0.0f;
+                        const int p = d >= 0 ? (int)dh.div((uint32_t)d) : -1;
+                        v[k] = (d >= 0 && d == p * f.H && p < f.Rb) ? gcol[p] : 0.0f;
                     }
                 }
             }
-            st_cs4(dst + 4 * q, v[0], v[1], v[2], v[3]);
+            st_cs4(dst + 4 * (int64_t)q, v[0], v[1], v[2], v[3]);
+            if (walk) {   // advance (i, rr, pp) by cstep columns
+                i += step_i;
+                int carry = 0;
+                if (i >= I) { i -= I; carry = 1; }
+                rr += step_rr + carry;
+                int carry2 = 0;
+                while (rr >= Bsplit) { rr -= Bsplit; ++carry2; }
+                pp += step_pp + carry2;
+            }
         }
         return;
     }
@@ -217,7 +321,7 @@ __device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* 
     }
 }
 
-__global__ void __launch_bounds__(kThreads) contract_kernel(const ContractArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) contract_kernel(const ContractArgs a) {
     extern __shared__ float scratch[];
     __shared__ PairCtx c;
     const int b = blockIdx.x;
@@ -245,15 +349,38 @@ __global__ void __launch_bounds__(kThreads) contract_kernel(const ContractArgs a
         }
     }
     __syncthreads();
-    const float* xc = a.x.cores + (a.x.offsets ? a.x.offsets[b] : (int64_t)b * a.x.train_elems);
-    const float* yc = a.y.cores + (a.y.offsets ? a.y.offsets[b] : (int64_t)b * a.y.train_elems);
+    const float* xg = a.x.cores + (a.x.offsets ? a.x.offsets[b] : (int64_t)b * a.x.train_elems);
+    const float* yg = a.y.cores + (a.y.offsets ? a.y.offsets[b] : (int64_t)b * a.y.train_elems);
     float* out = a.out + (a.out_offsets ? a.out_offsets[b] : (int64_t)b * a.out_pair_elems);
     float* TL = scratch + a.tl_off;
     float* TR = scratch + a.tr_off;
     float* tmp = scratch + a.tmp_off;
+    // stage both trains in shared memory when they fit (every core value is read many times)
+    const float* xc = xg;
+    const float* yc = yg;
+    const int64_t nx = c.xo[a.N], ny = c.yo[a.M];
+    if (a.stage_floats > 0 && nx + ny <= a.stage_floats) {
+        float* sx = scratch + a.stage_off;
+        float* sy = sx + nx;
+        for (int64_t e = threadIdx.x; e < nx; e += blockDim.x) sx[e] = __ldg(xg + e);
+        for (int64_t e = threadIdx.x; e < ny; e += blockDim.x) sy[e] = __ldg(yg + e);
+        xc = sx;
+        yc = sy;
+    }
     for (int l = 0; l < a.L; ++l) {
         const OutCore& oc = a.outc[l];
         int rows, cols;
+        if (threadIdx.x < 4) {   // magic-number divisors of this core, one per thread
+            const LadderEl& el = a.seq[oc.el];
+            const bool xf = el.kind == EL_XFREE;
+            const int I = xf ? a.xdims[el.mode] : a.ydims[el.mode];
+            const int Rn = xf ? c.rx[el.mode + 1] : c.ry[el.mode + 1];
+            const int H = xf ? c.ry[el.hold] : c.rx[el.hold];
+            const int d = threadIdx.x == 0 ? (c.orr[l] >= 4 ? c.orr[l] / 4 : 1)
+                        : threadIdx.x == 1 ? I : threadIdx.x == 2 ? (xf ? Rn : H) : H;
+            c.fd[threadIdx.x].init((uint32_t)d);
+        }
+        __syncthreads();
         if (oc.lt_count > 0) build_chain(a, c, xc, yc, oc.lt_first, oc.lt_count, TL, tmp, &rows, &cols);
         if (oc.rt_count > 0) {
             __syncthreads();

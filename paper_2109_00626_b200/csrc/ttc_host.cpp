@@ -524,7 +524,17 @@ ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const
     a.tr_off = (int32_t)p->tl_floats;
     a.tmp_off = (int32_t)(p->tl_floats + p->tr_floats);
     a.tmp_size = (int32_t)p->tmp_floats;
-    e = ttc::launch_contract(a, sizeof(float) * (size_t)p->scratch_floats, s);
+    // stage both trains of a pair in shared memory when the largest pair fits 40 KB
+    int64_t max_train = 0;
+    for (int b = 0; b < p->B; ++b) {
+        int64_t tx = 0, ty = 0;
+        for (int n = 0; n < p->N; ++n) tx += (int64_t)p->xranks[(size_t)b * (p->N + 1) + n] * p->xdims[n] * p->xranks[(size_t)b * (p->N + 1) + n + 1];
+        for (int m = 0; m < p->M; ++m) ty += (int64_t)p->yranks[(size_t)b * (p->M + 1) + m] * p->ydims[m] * p->yranks[(size_t)b * (p->M + 1) + m + 1];
+        max_train = std::max(max_train, tx + ty);
+    }
+    a.stage_off = (int32_t)p->scratch_floats;
+    a.stage_floats = max_train <= 10240 ? (int32_t)max_train : 0;
+    e = ttc::launch_contract(a, sizeof(float) * ((size_t)p->scratch_floats + (size_t)a.stage_floats), s);
     if (e != cudaSuccess) return cuda_fail(e, "ttc_contract launch");
     return TTC_OK;
 }

@@ -68,6 +68,7 @@ struct ContractArgs {
     int64_t  out_pair_elems;
     int32_t  tl_off, tr_off;      // shared-scratch offsets (floats) of the left / right transfer products
     int32_t  tmp_off, tmp_size;   // three temporaries of tmp_size floats for chains of >= 2 transfers
+    int32_t  stage_off, stage_floats;   // shared copy of the pair's two trains (0: read from global)
 };
 
 cudaError_t launch_contract(const ContractArgs& a, size_t smem_bytes, cudaStream_t s);
