@@ -208,8 +208,11 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     }
     const bool uniform_r16 = uniform && hx.urank == 16 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     const bool force_fast = kv && std::strcmp(kv, "fast") == 0;
+    const bool uniform_r64 = uniform && hx.urank == 64 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
         e = ttc::launch_inner_r16(a, s);
+    else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
+        e = ttc::launch_inner_r64(a, s);
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);
     else

@@ -33,6 +33,8 @@ bool        inner_fast_supported(const InnerArgs& a, int max_rank, bool uniform)
 cudaError_t launch_inner_fast(const InnerArgs& a, int max_rank, bool uniform, cudaStream_t s);
 bool        inner_r16_supported(const InnerArgs& a, bool uniform_r16);
 cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s);
+bool        inner_r64_supported(const InnerArgs& a, bool uniform_r64);
+cudaError_t launch_inner_r64(const InnerArgs& a, cudaStream_t s);
 
 // ---- tt_contract (ladder) ------------------------------------------------------------------------
 enum ElKind : int32_t { EL_XFREE = 1, EL_YFREE = 2, EL_T = 3 };
