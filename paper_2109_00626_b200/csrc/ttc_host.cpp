@@ -197,7 +197,7 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     const bool uniform = hx.uniform && hy.uniform && hx.urank == hy.urank;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    // TTC_KERNEL=generic|fast forces the general-shape / the ranks<=32 kernel (variant cross-checks in tests/)
+    // TTC_KERNEL=generic|fast|wpp forces the general-shape / CTA-per-pair / warp-per-pair kernel (cross-checks)
     const char* kv = std::getenv("TTC_KERNEL");
     const bool force_generic = kv && std::strcmp(kv, "generic") == 0;
     // uniform rank-16 trains with 16-byte aligned cores and trains: the specialised rank-16 kernel
@@ -208,11 +208,14 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     }
     const bool uniform_r16 = uniform && hx.urank == 16 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     const bool force_fast = kv && std::strcmp(kv, "fast") == 0;
+    const bool force_wpp = kv && std::strcmp(kv, "wpp") == 0;
     const bool uniform_r64 = uniform && hx.urank == 64 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
         e = ttc::launch_inner_r16(a, s);
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
         e = ttc::launch_inner_r64(a, s);
+    else if (force_wpp && ttc::inner_wpp_supported(a, mr))   // opt-in until its tile-specialised rewrite
+        e = ttc::launch_inner_wpp(a, mr, s);
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);
     else

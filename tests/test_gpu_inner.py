@@ -180,14 +180,15 @@ def test_edge_shapes():
         _check(Xs, Xs, got, range(B), "self")
 
 
-def test_kernel_variants_agree(monkeypatch):
-    """The specialised kernel and the general-shape kernel (TTC_KERNEL=generic) agree within fp32 rounding."""
-    for cfg, B in (("C2", 16), ("C5", 8), ("C1", 1)):
+@pytest.mark.parametrize("variant", ["generic", "fast", "wpp"])
+def test_kernel_variants_agree(monkeypatch, variant):
+    """Every tt_inner kernel (default dispatch vs TTC_KERNEL=generic / fast / wpp) agrees within fp32 rounding."""
+    for cfg, B in (("C2", 16), ("C5", 24), ("C1", 1), ("C4", 2)):
         X, Y = ttgen.config_batch(cfg, kind="corr", B=B)
-        fast = _run(X, Y)
-        monkeypatch.setenv("TTC_KERNEL", "generic")
-        gen = _run(X, Y)
+        ref = _run(X, Y)
+        monkeypatch.setenv("TTC_KERNEL", variant)
+        got = _run(X, Y)
         monkeypatch.delenv("TTC_KERNEL")
         for b in range(B):
             nrm = oracle.normaliser(X.train(b), Y.train(b))
-            assert abs(fast[b] - gen[b]) <= 1e-5 * nrm
+            assert abs(ref[b] - got[b]) <= 1e-5 * nrm, (cfg, b, ref[b], got[b])
