@@ -24,7 +24,9 @@ using namespace tc;
 
 constexpr int kWarps = 4;     // warps per CTA (independent)
 constexpr int kZS = 33;       // scratch row stride
+constexpr int kZsl = 32 * kZS; // offset of the lo half of the pre-split scratch
 constexpr int kDepth = 4;     // steps in flight per warp (issued, not yet computed)
+constexpr int kTail = 640;    // slack floats after a warp's region: unguarded reads of a partial M tile
 
 struct WppArgs {
     int ring;        // floats of one warp's ring
@@ -185,6 +187,157 @@ __device__ __forceinline__ void wpp_step(const float* F, int Fa, int Fb, const f
     __syncwarp();
 }
 
+// Full-tile variant of wpp_step for steps whose four bond ranks are multiples of 8 (C5's {8,16,24,32}):
+// K blocks and N tiles are exact, so fragment loads, B reads and Z writes need no guards; rows of a 16-row
+// M tile beyond the rank read padding / neighbouring data that only reaches output rows never read (the warp's
+// region is followed by kTail floats of slack so such reads stay inside shared memory).  Tiles are skipped by
+// warp-uniform branches, never by per-element predicates.
+__device__ __forceinline__ AFrag wpp_afrag_full(const float* G, int Ga, int I, int i, int u0, int v0, int g, int t) {
+    const float* p1 = G + u0 + 2 * t + Ga * (i + I * (v0 + g));
+    const float* p2 = p1 + Ga * I * 8;
+    const float2 x1 = *reinterpret_cast<const float2*>(p1);
+    const float2 x2 = *reinterpret_cast<const float2*>(p2);
+    AFrag f;
+    const float a[4] = {x1.x, x2.x, x1.y, x2.y};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        f.hi[k] = hi_bits(a[k]);
+        f.lo[k] = lo_bits(a[k], f.hi[k]);
+    }
+    return f;
+}
+
+// zsh / zsl: Z pre-split (hi, lo as the tensor core consumes them), written once per step.
+__device__ __forceinline__ void wpp_step_full(const float* F, int Fa, int Fb, const float* G, int Ga, int Gb, int I,
+                                              bool vf, uint32_t* zsh, uint32_t* zsl, int lane) {
+    const int lg = lane >> 2, t = lane & 3;
+    const int kf_n = Fa >> 3, ng_n = Ga >> 3, mq_n = (Fb + 15) >> 4, mg_n = (Gb + 15) >> 4, nf_n = Fb >> 3;
+    // scratch index of Z[g, f]: W-first g + kZS f, V-first f + kZS g
+    const int sg = vf ? kZS : 1, sf = vf ? 1 : kZS;
+    float acc[2][4][4];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[m][q][c] = 0.f;
+    for (int i = 0; i < I; ++i) {
+        // ---- GEMM-1: w[mq][ng] = sum_kf A_F(i, mq, kf) B_Z(kf, ng); two k-blocks per tensor-core group
+        float w[2][4][4];
+#pragma unroll
+        for (int mq = 0; mq < 2; ++mq) {
+            if (mq >= mq_n) break;
+#pragma unroll
+            for (int kp = 0; kp < 4; kp += 2) {
+                if (kp >= kf_n) break;
+                const bool two = kp + 1 < kf_n;
+                const AFrag A0 = wpp_afrag_full(F, Fa, I, i, 8 * kp, 16 * mq, lg, t);
+                AFrag A1 = A0;
+                if (two) A1 = wpp_afrag_full(F, Fa, I, i, 8 * kp + 8, 16 * mq, lg, t);
+#pragma unroll
+                for (int ng = 0; ng < 4; ++ng) {
+                    if (ng >= ng_n) break;
+                    const int gg = 8 * ng + lg, f0 = 8 * kp + 2 * t;
+                    const int i0 = gg * sg + f0 * sf, i1 = i0 + sf;
+                    BFrag B0;
+                    B0.hi[0] = zsh[i0]; B0.hi[1] = zsh[i1]; B0.lo[0] = zsl[i0]; B0.lo[1] = zsl[i1];
+                    float tg[4];
+                    mma3<true>(tg, A0, B0);
+                    if (two) {
+                        const int j0 = i0 + 8 * sf, j1 = j0 + sf;
+                        BFrag B1;
+                        B1.hi[0] = zsh[j0]; B1.hi[1] = zsh[j1]; B1.lo[0] = zsl[j0]; B1.lo[1] = zsl[j1];
+                        mma3<false>(tg, A1, B1);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) w[mq][ng][c] = (kp == 0) ? tg[c] : w[mq][ng][c] + tg[c];
+                }
+            }
+        }
+        // ---- GEMM-2: acc[mg][nf] += sum_kg A_G(i, mg, kg) B_W(kg, nf), B_W(kg, nf) = w[nf/2][kg][2 (nf%2) + j]
+#pragma unroll
+        for (int mg = 0; mg < 2; ++mg) {
+            if (mg >= mg_n) break;
+#pragma unroll
+            for (int kp = 0; kp < 4; kp += 2) {
+                if (kp >= ng_n) break;
+                const bool two = kp + 1 < ng_n;
+                const AFrag A0 = wpp_afrag_full(G, Ga, I, i, 8 * kp, 16 * mg, lg, t);
+                AFrag A1 = A0;
+                if (two) A1 = wpp_afrag_full(G, Ga, I, i, 8 * kp + 8, 16 * mg, lg, t);
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf) {
+                    if (nf >= nf_n) break;
+                    const BFrag B0 = split_b(w[nf >> 1][kp][2 * (nf & 1)], w[nf >> 1][kp][2 * (nf & 1) + 1]);
+                    float tg[4];
+                    mma3<true>(tg, A0, B0);
+                    if (two) {
+                        const BFrag B1 = split_b(w[nf >> 1][kp + 1][2 * (nf & 1)], w[nf >> 1][kp + 1][2 * (nf & 1) + 1]);
+                        mma3<false>(tg, A1, B1);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[mg][nf][c] += tg[c];
+                }
+            }
+        }
+    }
+    __syncwarp();   // every lane has read the old Z
+    // ---- Z'[g', f'] -> canonical scratch, split once; rows g' >= Gb of a partial M tile are written too
+#pragma unroll
+    for (int mg = 0; mg < 2; ++mg) {
+        if (mg >= mg_n) break;
+#pragma unroll
+        for (int nf = 0; nf < 4; ++nf) {
+            if (nf >= nf_n) break;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int gg = 16 * mg + lg + 8 * (c >> 1), ff = 8 * nf + 2 * t + (c & 1);
+                const uint32_t h = hi_bits(acc[mg][nf][c]);
+                zsh[gg * sg + ff * sf] = h;
+                zsl[gg * sg + ff * sf] = lo_bits(acc[mg][nf][c], h);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// Boundary steps on the FP32 pipe (rank-1 bonds make every tensor-core tile mostly padding).
+// First step (R = P = 1): Z_1[s, q] = sum_i X_1[0,i,s] Y_1[0,i,q] -- Eq. 12's K -- into the canonical scratch.
+template <bool SPLIT>
+__device__ __forceinline__ void wpp_first(const float* X, const float* Y, int S, int Q, int I, float* zs, int lane) {
+    for (int e = lane; e < S * Q; e += 32) {
+        const int sidx = e % S, q = e / S;
+        float d = 0.f;
+        for (int i = 0; i < I; ++i) d = fmaf(X[i + I * sidx], Y[i + I * q], d);
+        if (SPLIT) {   // pre-split scratch: hi in zs, lo in zs + kZsl
+            const uint32_t h = hi_bits(d);
+            reinterpret_cast<uint32_t*>(zs)[sidx + kZS * q] = h;
+            reinterpret_cast<uint32_t*>(zs)[kZsl + sidx + kZS * q] = lo_bits(d, h);
+        } else {
+            zs[sidx + kZS * q] = d;
+        }
+    }
+    __syncwarp();
+}
+// Last step (S = Q = 1): Z_N = sum_{r,p} Z[r,p] sum_i X_N[r,i,0] Y_N[p,i,0] (warp-reduced, fixed order).
+// With R = P = 1 (N == 1) this is the dot product sum_i x_i y_i.
+template <bool SPLIT>
+__device__ __forceinline__ float wpp_last(const float* X, const float* Y, int R, int P, int I, bool first, const float* zs,
+                                          int lane) {
+    float v = 0.f;
+    for (int e = lane; e < R * P; e += 32) {
+        const int r = e % R, p = e / R;
+        float d = 0.f;
+        for (int i = 0; i < I; ++i) d = fmaf(X[r + R * i], Y[p + P * i], d);
+        float z = 1.0f;
+        if (!first) z = SPLIT ? zs[r + kZS * p] + zs[kZsl + r + kZS * p] : zs[r + kZS * p];   // hi + lo = Z exactly
+        v = fmaf(z, d, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // Per-warp cursor over this warp's (pair, step) sequence.
 struct WCursor {
     int k, b, n, R, P;
@@ -209,17 +362,19 @@ struct InFlight {
     unsigned end;       // monotone ring position after this step
 };
 
-__global__ void __launch_bounds__(32 * kWarps) inner_wpp_kernel(const InnerArgs a, const WppArgs w) {
+template <bool FULL>
+__global__ void __launch_bounds__(32 * kWarps, FULL ? 3 : 2) inner_wpp_kernel(const InnerArgs a, const WppArgs w) {
     extern __shared__ __align__(16) float smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* ring = smem + warp * w.warp_floats;
     float* zs = ring + w.ring;
-    InFlight* q = reinterpret_cast<InFlight*>(zs + ((32 * kZS + 3) & ~3));   // kDepth entries, warp-private
+    InFlight* q = reinterpret_cast<InFlight*>(zs + 2 * ((32 * kZS + 3) & ~3));   // kDepth entries, warp-private
     const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
     WCursor ic;
     ic.k = 0;
     wc_pair(a, ic, gw, nw);
     unsigned head = 0, tail = 0;   // monotone ring positions (floats)
+    unsigned head_off = 0;         // head's offset inside the ring
     int qh = 0, qn = 0;            // in-flight queue: oldest entry index, count
     const unsigned RING = (unsigned)w.ring;
     while (true) {
@@ -229,11 +384,11 @@ __global__ void __launch_bounds__(32 * kWarps) inner_wpp_kernel(const InnerArgs 
             const int S = wrank(a.x, ic.b, a.N, ic.n + 1), Q = wrank(a.y, ic.b, a.N, ic.n + 1);
             const int nx = ic.R * I * S, ny = ic.P * I * Q;
             const unsigned need = (unsigned)((nx + 3) & ~3) + (unsigned)((ny + 3) & ~3);
-            unsigned start = head;
-            if ((start % RING) + need > RING) start = (start / RING + 1) * RING;   // do not wrap a step
-            if (qn == 0) tail = start;                                              // empty ring: the skip is free
-            if (start + need - tail > RING) break;                                  // no room yet
-            float* dst = ring + (start % RING);
+            unsigned start = head, start_off = head_off;
+            if (start_off + need > RING) { start += RING - start_off; start_off = 0; }   // do not wrap a step
+            if (qn == 0) tail = start;                                                  // empty ring: the skip is free
+            if (start + need - tail > RING) break;                                      // no room yet
+            float* dst = ring + start_off;
             const float* xs = a.x.cores + ic.xo;
             const float* ys = a.y.cores + ic.yo;
             const int nxp = (nx + 3) & ~3;
@@ -247,13 +402,14 @@ __global__ void __launch_bounds__(32 * kWarps) inner_wpp_kernel(const InnerArgs 
             cp_commit();
             if (lane == 0) {
                 InFlight f;
-                f.start = (int)(start % RING);
+                f.start = (int)start_off;
                 f.b = ic.b; f.n = ic.n; f.R = ic.R; f.P = ic.P; f.S = S; f.Q = Q; f.I = I;
                 f.end = start + need;
                 q[(qh + qn) % kDepth] = f;
             }
             ++qn;
             head = start + need;
+            head_off = start_off + need;
             ic.xo += nx;
             ic.yo += ny;
             ic.R = S;
@@ -270,13 +426,21 @@ __global__ void __launch_bounds__(32 * kWarps) inner_wpp_kernel(const InnerArgs 
         const InFlight f = q[qh];
         const float* X = ring + f.start;
         const float* Y = X + ((f.R * f.I * f.S + 3) & ~3);
-        if (f.n == 0) {   // Z_0 = [1]
-            if (lane == 0) zs[0] = 1.0f;
-            __syncwarp();
-        }
         const bool vf = (f.R * f.P * f.S + f.P * f.S * f.Q) < (f.R * f.P * f.Q + f.R * f.S * f.Q);
-        if (vf) wpp_step(X, f.R, f.S, Y, f.P, f.Q, f.I, true, zs, lane);
-        else wpp_step(Y, f.P, f.Q, X, f.R, f.S, f.I, false, zs, lane);
+        if (f.n == a.N - 1) {
+            const float v = wpp_last<FULL>(X, Y, f.R, f.P, f.I, f.n == 0, zs, lane);
+            if (lane == 0) zs[0] = v;
+            __syncwarp();
+        } else if (f.n == 0) {
+            wpp_first<FULL>(X, Y, f.S, f.Q, f.I, zs, lane);
+        } else if (FULL) {   // every interior rank of the batch is a multiple of 8 (host-checked)
+            uint32_t* zh = reinterpret_cast<uint32_t*>(zs);
+            if (vf) wpp_step_full(X, f.R, f.S, Y, f.P, f.Q, f.I, true, zh, zh + kZsl, lane);
+            else wpp_step_full(Y, f.P, f.Q, X, f.R, f.S, f.I, false, zh, zh + kZsl, lane);
+        } else {
+            if (vf) wpp_step(X, f.R, f.S, Y, f.P, f.Q, f.I, true, zs, lane);
+            else wpp_step(Y, f.P, f.Q, X, f.R, f.S, f.I, false, zs, lane);
+        }
 #ifdef TTC_WPP_DEBUG
         if (lane == 0 && f.b == 0)
             printf("n=%d R=%d P=%d S=%d Q=%d I=%d start=%d end=%u head=%u tail=%u qn=%d vf=%d z00=%g\n", f.n, f.R, f.P, f.S,
@@ -304,29 +468,34 @@ bool inner_wpp_supported(const InnerArgs& a, int max_rank) {
     if (max_rank > 32 || a.N < 1) return false;
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = std::max(max_dim, (int)a.dims[n]);
-    const int64_t warp_floats = wpp_ring(max_rank, max_dim) + ((32 * kZS + 3) & ~3) + kDepth * (int64_t)sizeof(InFlight) / 4;
+    const int64_t warp_floats = wpp_ring(max_rank, max_dim) + 2 * ((32 * kZS + 3) & ~3) + kDepth * (int64_t)sizeof(InFlight) / 4 + kTail;
     return sizeof(float) * warp_floats * kWarps <= 200 * 1024;
 }
 
-cudaError_t launch_inner_wpp(const InnerArgs& a, int max_rank, cudaStream_t s) {
+template <bool FULL>
+cudaError_t launch_wpp_t(const InnerArgs& a, int max_rank, cudaStream_t s) {
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = std::max(max_dim, (int)a.dims[n]);
     WppArgs w;
     w.ring = (int)wpp_ring(max_rank, max_dim);
-    w.warp_floats = w.ring + ((32 * kZS + 3) & ~3) + (int)(kDepth * sizeof(InFlight) / 4);
+    w.warp_floats = w.ring + 2 * ((32 * kZS + 3) & ~3) + (int)(kDepth * sizeof(InFlight) / 4) + kTail;
     const size_t smem = sizeof(float) * (size_t)w.warp_floats * kWarps;
-    cudaError_t e = cudaFuncSetAttribute(inner_wpp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(inner_wpp_kernel<FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_wpp_kernel, 32 * kWarps, smem)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_wpp_kernel<FULL>, 32 * kWarps, smem)) != cudaSuccess)
         return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int want = (a.B + kWarps - 1) / kWarps;
     const int grid = want < sms * per_sm ? want : sms * per_sm;
-    inner_wpp_kernel<<<grid, 32 * kWarps, smem, s>>>(a, w);
+    inner_wpp_kernel<FULL><<<grid, 32 * kWarps, smem, s>>>(a, w);
     return cudaGetLastError();
+}
+
+cudaError_t launch_inner_wpp(const InnerArgs& a, int max_rank, bool ranks_mult8, cudaStream_t s) {
+    return ranks_mult8 ? launch_wpp_t<true>(a, max_rank, s) : launch_wpp_t<false>(a, max_rank, s);
 }
 
 }  // namespace ttc

@@ -36,6 +36,7 @@ struct HostTrain {
     bool uniform = true;
     int urank = 1;
     int max_rank = 1;
+    bool mult8 = true;                 // every interior rank is a multiple of 8
     int64_t train_elems_uniform = 0;   // uniform ranks: elements per train
 
     int rank(int b, int n) const {
@@ -66,6 +67,7 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
             if (t->uniform_rank > TTC_MAX_RANK)
                 return fail(TTC_ERR_UNSUPPORTED, "%s: uniform_rank = %d > %d", name, t->uniform_rank, TTC_MAX_RANK);
             h->urank = t->uniform_rank;
+            h->mult8 = (h->urank & 7) == 0;
         }
         h->max_rank = t->order > 1 ? h->urank : 1;
     } else {
@@ -81,6 +83,7 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
                 if (r[n] > TTC_MAX_RANK)
                     return fail(TTC_ERR_UNSUPPORTED, "%s pair %d: rank R_%d = %d > %d", name, b, n, r[n], TTC_MAX_RANK);
                 mr = std::max(mr, (int)r[n]);
+                if (r[n] & 7) h->mult8 = false;
             }
         }
         h->max_rank = mr;
@@ -215,7 +218,7 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
         e = ttc::launch_inner_r64(a, s);
     else if (force_wpp && ttc::inner_wpp_supported(a, mr))   // opt-in until its tile-specialised rewrite
-        e = ttc::launch_inner_wpp(a, mr, s);
+        e = ttc::launch_inner_wpp(a, mr, hx.mult8 && hy.mult8, s);
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);
     else

@@ -192,3 +192,30 @@ def test_kernel_variants_agree(monkeypatch, variant):
         for b in range(B):
             nrm = oracle.normaliser(X.train(b), Y.train(b))
             assert abs(ref[b] - got[b]) <= 1e-5 * nrm, (cfg, b, ref[b], got[b])
+
+
+def test_sharded_inner_nccl_single_rank():
+    """dist.sharded_inner over an NCCL group (world size 1 on this box): partition + shard views +
+    all_gather_into_tensor + compaction reproduce the unsharded call bitwise."""
+    import os
+    import torch.distributed as dist
+    from paper_2109_00626_b200 import dist as tdist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        X, Y = ttgen.config_batch("C5", kind="iid", B=40)
+        XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+        full = ttc.ttc_inner(XD, YD)
+        got, bounds = tdist.sharded_inner(XD, YD)
+        torch.cuda.synchronize()
+        assert list(bounds) == [0, 40]
+        assert torch.equal(got, full)
+        # shard views of a 4-way plan, run one after another, gathered by hand
+        mac, _ = ttc.ttc_pair_cost(XD, YD)
+        b4 = tdist.shard_bounds(mac, 4)
+        parts = [ttc.ttc_inner(tdist.shard_view(XD, int(b4[r]), int(b4[r + 1])),
+                               tdist.shard_view(YD, int(b4[r]), int(b4[r + 1]))) for r in range(4)]
+        assert torch.equal(torch.cat(parts), full)
+    finally:
+        dist.destroy_process_group()
