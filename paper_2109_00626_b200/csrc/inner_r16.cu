@@ -108,10 +108,7 @@ __device__ __forceinline__ void r16_units(const float* F, const float* G, int ps
             A[kf] = split_a_trunc(fa);
         }
 #pragma unroll
-        for (int ng = 0; ng < 2; ++ng) {
-            mma3<true>(w[x][ng], A[0], zb[0][ng]);
-            mma3<false>(w[x][ng], A[1], zb[1][ng]);
-        }
+        for (int ng = 0; ng < 2; ++ng) mma6<true>(w[x][ng], A[0], zb[0][ng], A[1], zb[1][ng]);
     }
 #pragma unroll
     for (int x = 0; x < U; ++x) {   // GEMM-2: Z'[s, q] += sum_r X[r, i, s] W[r, i, q]
@@ -130,8 +127,7 @@ __device__ __forceinline__ void r16_units(const float* F, const float* G, int ps
             const BFrag B0 = split_b(w[x][0][2 * h], w[x][0][2 * h + 1]);
             const BFrag B1 = split_b(w[x][1][2 * h], w[x][1][2 * h + 1]);
             float tg[4];
-            mma3<true>(tg, A[0], B0);
-            mma3<false>(tg, A[1], B1);
+            mma6<true>(tg, A[0], B0, A[1], B1);
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[h][c] += tg[c];
         }

@@ -235,8 +235,7 @@ __global__ void __maxnreg__(168) inner_r64_kernel(const InnerArgs a, const R64La
                     for (int x = 0; x < 2; ++x) {
                         if (x == 1 && !two) break;
                         float tg[4];
-                        mma3<true>(tg, A[x][0], B[0]);
-                        mma3<false>(tg, A[x][1], B[1]);
+                        mma6<true>(tg, A[x][0], B[0], A[x][1], B[1]);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) w[x][ng][c] = (kf == 0) ? tg[c] : w[x][ng][c] + tg[c];
                     }

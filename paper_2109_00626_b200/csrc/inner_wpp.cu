@@ -207,6 +207,88 @@ __device__ __forceinline__ AFrag wpp_afrag_full(const float* G, int Ga, int I, i
     return f;
 }
 
+// U consecutive slices i0 .. i0+U-1 of a full-tile step in lockstep (the slices' GEMM chains are independent until
+// they reach acc).  U = 1 is used: U = 2 spilled registers and measured slower on C5.
+template <int U>
+__device__ __forceinline__ void wpp_slices(const float* F, int Fa, const float* G, int Ga, int I, int i0, int kf_n, int ng_n,
+                                           int mq_n, int mg_n, int nf_n, int sg, int sf, const uint32_t* zsh,
+                                           const uint32_t* zsl, int lg, int t, float (&acc)[2][4][4]) {
+    // ---- GEMM-1: w[x][mq][ng] = sum_kf A_F(i0+x, mq, kf) B_Z(kf, ng); two k-blocks per tensor-core group
+    float w[U][2][4][4];
+#pragma unroll
+    for (int mq = 0; mq < 2; ++mq) {
+        if (mq >= mq_n) break;
+#pragma unroll
+        for (int kp = 0; kp < 4; kp += 2) {
+            if (kp >= kf_n) break;
+            const bool two = kp + 1 < kf_n;
+            AFrag A0[U], A1[U];
+#pragma unroll
+            for (int x = 0; x < U; ++x) {
+                A0[x] = wpp_afrag_full(F, Fa, I, i0 + x, 8 * kp, 16 * mq, lg, t);
+                A1[x] = A0[x];
+                if (two) A1[x] = wpp_afrag_full(F, Fa, I, i0 + x, 8 * kp + 8, 16 * mq, lg, t);
+            }
+#pragma unroll
+            for (int ng = 0; ng < 4; ++ng) {
+                if (ng >= ng_n) break;
+                const int gg = 8 * ng + lg, f0 = 8 * kp + 2 * t;
+                const int i0z = gg * sg + f0 * sf, i1z = i0z + sf;
+                BFrag B0, B1;
+                B0.hi[0] = zsh[i0z]; B0.hi[1] = zsh[i1z]; B0.lo[0] = zsl[i0z]; B0.lo[1] = zsl[i1z];
+                if (two) {
+                    const int j0 = i0z + 8 * sf, j1 = j0 + sf;
+                    B1.hi[0] = zsh[j0]; B1.hi[1] = zsh[j1]; B1.lo[0] = zsl[j0]; B1.lo[1] = zsl[j1];
+                }
+#pragma unroll
+                for (int x = 0; x < U; ++x) {
+                    float tg[4];
+                    if (two) mma6<true>(tg, A0[x], B0, A1[x], B1);
+                    else mma3<true>(tg, A0[x], B0);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) w[x][mq][ng][c] = (kp == 0) ? tg[c] : w[x][mq][ng][c] + tg[c];
+                }
+            }
+        }
+    }
+    // ---- GEMM-2: acc[mg][nf] += sum_x sum_kg A_G(i0+x, mg, kg) B_W(x, kg, nf)
+#pragma unroll
+    for (int mg = 0; mg < 2; ++mg) {
+        if (mg >= mg_n) break;
+#pragma unroll
+        for (int kp = 0; kp < 4; kp += 2) {
+            if (kp >= ng_n) break;
+            const bool two = kp + 1 < ng_n;
+            AFrag A0[U], A1[U];
+#pragma unroll
+            for (int x = 0; x < U; ++x) {
+                A0[x] = wpp_afrag_full(G, Ga, I, i0 + x, 8 * kp, 16 * mg, lg, t);
+                A1[x] = A0[x];
+                if (two) A1[x] = wpp_afrag_full(G, Ga, I, i0 + x, 8 * kp + 8, 16 * mg, lg, t);
+            }
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf) {
+                if (nf >= nf_n) break;
+                float tg[U][4];
+#pragma unroll
+                for (int x = 0; x < U; ++x) {
+                    const BFrag B0 = split_b(w[x][nf >> 1][kp][2 * (nf & 1)], w[x][nf >> 1][kp][2 * (nf & 1) + 1]);
+                    if (two) {
+                        const BFrag B1 = split_b(w[x][nf >> 1][kp + 1][2 * (nf & 1)], w[x][nf >> 1][kp + 1][2 * (nf & 1) + 1]);
+                        mma6<true>(tg[x], A0[x], B0, A1[x], B1);
+                    } else {
+                        mma3<true>(tg[x], A0[x], B0);
+                    }
+                }
+#pragma unroll
+                for (int x = 0; x < U; ++x)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[mg][nf][c] += tg[x][c];
+            }
+        }
+    }
+}
+
 // zsh / zsl: Z pre-split (hi, lo as the tensor core consumes them), written once per step.
 __device__ __forceinline__ void wpp_step_full(const float* F, int Fa, int Fb, const float* G, int Ga, int Gb, int I,
                                               bool vf, uint32_t* zsh, uint32_t* zsl, int lane) {
@@ -221,66 +303,7 @@ __device__ __forceinline__ void wpp_step_full(const float* F, int Fa, int Fb, co
         for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[m][q][c] = 0.f;
-    for (int i = 0; i < I; ++i) {
-        // ---- GEMM-1: w[mq][ng] = sum_kf A_F(i, mq, kf) B_Z(kf, ng); two k-blocks per tensor-core group
-        float w[2][4][4];
-#pragma unroll
-        for (int mq = 0; mq < 2; ++mq) {
-            if (mq >= mq_n) break;
-#pragma unroll
-            for (int kp = 0; kp < 4; kp += 2) {
-                if (kp >= kf_n) break;
-                const bool two = kp + 1 < kf_n;
-                const AFrag A0 = wpp_afrag_full(F, Fa, I, i, 8 * kp, 16 * mq, lg, t);
-                AFrag A1 = A0;
-                if (two) A1 = wpp_afrag_full(F, Fa, I, i, 8 * kp + 8, 16 * mq, lg, t);
-#pragma unroll
-                for (int ng = 0; ng < 4; ++ng) {
-                    if (ng >= ng_n) break;
-                    const int gg = 8 * ng + lg, f0 = 8 * kp + 2 * t;
-                    const int i0 = gg * sg + f0 * sf, i1 = i0 + sf;
-                    BFrag B0;
-                    B0.hi[0] = zsh[i0]; B0.hi[1] = zsh[i1]; B0.lo[0] = zsl[i0]; B0.lo[1] = zsl[i1];
-                    float tg[4];
-                    mma3<true>(tg, A0, B0);
-                    if (two) {
-                        const int j0 = i0 + 8 * sf, j1 = j0 + sf;
-                        BFrag B1;
-                        B1.hi[0] = zsh[j0]; B1.hi[1] = zsh[j1]; B1.lo[0] = zsl[j0]; B1.lo[1] = zsl[j1];
-                        mma3<false>(tg, A1, B1);
-                    }
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) w[mq][ng][c] = (kp == 0) ? tg[c] : w[mq][ng][c] + tg[c];
-                }
-            }
-        }
-        // ---- GEMM-2: acc[mg][nf] += sum_kg A_G(i, mg, kg) B_W(kg, nf), B_W(kg, nf) = w[nf/2][kg][2 (nf%2) + j]
-#pragma unroll
-        for (int mg = 0; mg < 2; ++mg) {
-            if (mg >= mg_n) break;
-#pragma unroll
-            for (int kp = 0; kp < 4; kp += 2) {
-                if (kp >= ng_n) break;
-                const bool two = kp + 1 < ng_n;
-                const AFrag A0 = wpp_afrag_full(G, Ga, I, i, 8 * kp, 16 * mg, lg, t);
-                AFrag A1 = A0;
-                if (two) A1 = wpp_afrag_full(G, Ga, I, i, 8 * kp + 8, 16 * mg, lg, t);
-#pragma unroll
-                for (int nf = 0; nf < 4; ++nf) {
-                    if (nf >= nf_n) break;
-                    const BFrag B0 = split_b(w[nf >> 1][kp][2 * (nf & 1)], w[nf >> 1][kp][2 * (nf & 1) + 1]);
-                    float tg[4];
-                    mma3<true>(tg, A0, B0);
-                    if (two) {
-                        const BFrag B1 = split_b(w[nf >> 1][kp + 1][2 * (nf & 1)], w[nf >> 1][kp + 1][2 * (nf & 1) + 1]);
-                        mma3<false>(tg, A1, B1);
-                    }
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[mg][nf][c] += tg[c];
-                }
-            }
-        }
-    }
+    for (int i = 0; i < I; ++i) wpp_slices<1>(F, Fa, G, Ga, I, i, kf_n, ng_n, mq_n, mg_n, nf_n, sg, sf, zsh, zsl, lg, t, acc);
     __syncwarp();   // every lane has read the old Z
     // ---- Z'[g', f'] -> canonical scratch, split once; rows g' >= Gb of a partial M tile are written too
 #pragma unroll
@@ -363,7 +386,7 @@ struct InFlight {
 };
 
 template <bool FULL>
-__global__ void __launch_bounds__(32 * kWarps, FULL ? 3 : 2) inner_wpp_kernel(const InnerArgs a, const WppArgs w) {
+__global__ void __launch_bounds__(32 * kWarps, 2) inner_wpp_kernel(const InnerArgs a, const WppArgs w) {
     extern __shared__ __align__(16) float smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* ring = smem + warp * w.warp_floats;

@@ -118,6 +118,20 @@ __device__ __forceinline__ void mma3(float (&d)[4], const AFrag& A, const BFrag&
     mma_acc(d, A.hi, B.hi[0], B.hi[1]);
 }
 
+// d (=) A0 B0 + A1 B1 over two k8 blocks, 3xTF32, ordered so the four small cross terms accumulate first
+// and the two large hi*hi products last: the tensor core's truncating accumulation then loses at most two
+// large-magnitude roundings per group.
+template <bool FIRST>
+__device__ __forceinline__ void mma6(float (&d)[4], const AFrag& A0, const BFrag& B0, const AFrag& A1, const BFrag& B1) {
+    if (FIRST) mma_zero(d, A0.lo, B0.hi[0], B0.hi[1]);
+    else mma_acc(d, A0.lo, B0.hi[0], B0.hi[1]);
+    mma_acc(d, A0.hi, B0.lo[0], B0.lo[1]);
+    mma_acc(d, A1.lo, B1.hi[0], B1.hi[1]);
+    mma_acc(d, A1.hi, B1.lo[0], B1.lo[1]);
+    mma_acc(d, A0.hi, B0.hi[0], B0.hi[1]);
+    mma_acc(d, A1.hi, B1.hi[0], B1.hi[1]);
+}
+
 __host__ __device__ __forceinline__ int plane_stride(int floats) {   // >= floats, multiple of 4, = 8 mod 32
     int ps = (floats + 3) & ~3;
     ps += (8 - (ps & 31) + 32) & 31;

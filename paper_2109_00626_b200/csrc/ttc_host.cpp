@@ -217,8 +217,8 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
         e = ttc::launch_inner_r16(a, s);
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
         e = ttc::launch_inner_r64(a, s);
-    else if (force_wpp && ttc::inner_wpp_supported(a, mr))   // opt-in until its tile-specialised rewrite
-        e = ttc::launch_inner_wpp(a, mr, hx.mult8 && hy.mult8, s);
+    else if (!force_generic && !force_fast && (force_wpp || (hx.mult8 && hy.mult8)) && ttc::inner_wpp_supported(a, mr))
+        e = ttc::launch_inner_wpp(a, mr, hx.mult8 && hy.mult8, s);   // warp per pair (ranks multiple of 8: full tiles)
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);
     else
