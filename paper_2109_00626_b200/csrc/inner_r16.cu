@@ -25,6 +25,10 @@ constexpr int kCW = 8;          // compute warps
 constexpr int kCT = 32 * kCW;   // compute threads = zfrag slots (2 x 2 fragments x 64)
 constexpr int kPart = 2 * 32 * 4;   // floats of one warp's partial Z' (2 n-tiles, fragment-native)
 constexpr int kEnd = 1 << 30;
+#ifndef TTC_R16_STAGES
+#define TTC_R16_STAGES 3
+#endif
+constexpr int kStages = TTC_R16_STAGES;   // TMA ring depth (steps in flight per CTA)
 
 struct R16Step {
     int b, n, I, flags;   // flags: 1 first step, 2 last step, kEnd: no more steps
@@ -136,19 +140,19 @@ __device__ __forceinline__ void r16_units(const float* F, const float* G, int ps
 
 __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Layout lay) {
     extern __shared__ __align__(128) float smem[];
-    __shared__ __align__(8) uint64_t full[2], empty[2];
-    __shared__ __align__(16) R16Step ring[4];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    __shared__ __align__(16) R16Step ring[8];
     __shared__ float red[kCW];
     float* stages = smem;
-    float* zpart = smem + 2 * lay.stage_floats;   // [kCW][2 n-tiles][32 lanes][4]
+    float* zpart = smem + kStages * lay.stage_floats;   // [kCW][2 n-tiles][32 lanes][4]
     float* zfrag = zpart + kCW * kPart;           // [kf][ng][32 lanes][2]: B fragments of Z for the next step
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(&empty[0], kCW);
-        mbar_init(&empty[1], kCW);
+        for (int k = 0; k < kStages; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kCW);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -158,16 +162,16 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
         ic.k = 0;
         r16_pair(a, ic);
         for (int j = 0;; ++j) {
-            const int st = j & 1;
-            if (j >= 2) mbar_wait(&empty[st], ((j >> 1) - 1) & 1);
+            const int st = j % kStages;
+            if (j >= kStages) mbar_wait(&empty[st], ((j / kStages) - 1) & 1);
             if (!ic.valid) {
                 if (lane == 0) {
-                    ring[j & 3].flags = kEnd;
+                    ring[j & 7].flags = kEnd;
                     mbar_arrive(&full[st]);
                 }
                 break;
             }
-            r16_issue(a, ic, &ring[j & 3], stages + st * lay.stage_floats, &full[st], lay);
+            r16_issue(a, ic, &ring[j & 7], stages + st * lay.stage_floats, &full[st], lay);
         }
         return;
     }
@@ -182,9 +186,9 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
     const int src = ((zf >> 3) * 32 + ((zg & 7) << 2) + ((zf & 7) >> 1)) * 4 + ((zg >> 3) << 1) + (zf & 1);
 
     for (int j = 0;; ++j) {
-        const int st = j & 1;
-        mbar_wait(&full[st], (j >> 1) & 1);
-        const R16Step si = ring[j & 3];
+        const int st = j % kStages;
+        mbar_wait(&full[st], (j / kStages) & 1);
+        const R16Step si = ring[j & 7];
         if (si.flags == kEnd) break;
         const float* X = stages + st * lay.stage_floats;
         const float* Y = X + lay.x_floats;
@@ -270,8 +274,8 @@ bool inner_r16_supported(const InnerArgs& a, bool uniform_r16) {
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
     // two stages of 2 x 16 padded planes + partials + fragments
-    const size_t smem = sizeof(float) * (2 * (size_t)2 * 16 * plane_stride(16 * max_dim) + kCW * kPart + kCT);
-    return smem <= 110 * 1024;   // two CTAs per SM
+    const size_t smem = sizeof(float) * (kStages * (size_t)2 * 16 * plane_stride(16 * max_dim) + kCW * kPart + kCT);
+    return smem <= 112 * 1024;   // two CTAs per SM
 }
 
 cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s) {
@@ -281,7 +285,7 @@ cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s) {
     lay.ps_max = plane_stride(16 * max_dim);
     lay.x_floats = 16 * lay.ps_max;
     lay.stage_floats = 2 * lay.x_floats;
-    const size_t smem = sizeof(float) * (2 * (size_t)lay.stage_floats + kCW * kPart + kCT);
+    const size_t smem = sizeof(float) * (kStages * (size_t)lay.stage_floats + kCW * kPart + kCT);
     cudaError_t e = cudaFuncSetAttribute(inner_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
