@@ -180,6 +180,24 @@ def test_edge_shapes():
         _check(Xs, Xs, got, range(B), "self")
 
 
+@pytest.mark.parametrize("dims", [(16, 16), (4, 16, 16), (16, 16, 16), (3, 5, 16, 7, 2), (13, 9, 11, 1),
+                                  (1, 8, 1, 8, 1, 8), (6, 12, 16, 10, 14, 4, 2)])
+def test_uniform_rank16_shapes(dims):
+    """The uniform rank-16 kernel (first / last cores from L2, interior cores through the TMA ring) on mixed
+    mode sizes: fewer slices than warps, odd slice counts, I = 1 cores, boundary I not a multiple of 4, a single
+    interior core (N = 3), and N = 2 (no interior core: served by another kernel)."""
+    rng = np.random.default_rng(sum(dims))
+    B = 37
+    N = len(dims)
+    r = np.tile(np.array([1] + [16] * (N - 1) + [1], np.int32), (B, 1))
+    X = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, r, dims, "geo")
+    Y = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 1, 0, r, dims, "geo")
+    got = _run(X, Y)
+    _check(X, Y, got, range(B), "edge")
+    got = _run(X, X)
+    _check(X, X, got, range(B), "self")
+
+
 @pytest.mark.parametrize("variant", ["generic", "fast", "wpp"])
 def test_kernel_variants_agree(monkeypatch, variant):
     """Every tt_inner kernel (default dispatch vs TTC_KERNEL=generic / fast / wpp) agrees within fp32 rounding."""
