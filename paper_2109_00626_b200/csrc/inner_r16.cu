@@ -1,22 +1,18 @@
 // inner_r16.cu -- tt_inner specialised for batches whose trains all have the rank profile (1, 16, ..., 16, 1)
 // (BASELINE.json C2: N = 8, I = 16, R = 16).  Same sweep as ttc.h / inner_fast.cu:
 //   Z_0 = [1],  Z_n = sum_i X_n[:, i, :]^T Z_{n-1} Y_n[:, i, :],  out = Z_N.
-// Persistent CTAs, warp-specialised:
+// Persistent CTAs (two per SM), warp-specialised:
 //   * producer warp: TMA bulk copies (cp.async.bulk) of each INTERIOR step's two cores into a kStages-deep ring
-//     (one copy per plane into padded planes), full/empty mbarriers; the two rank-1 boundary cores of a pair
-//     (1 KB each per train for I = 16) are only prefetched into L2 (cp.async.bulk.prefetch.L2) -- a boundary
-//     step in the ring would occupy a whole stage for 1/16 of its data and leave the next pair's first
-//     interior stage issued just one short step ahead of its use (an exposed HBM latency per pair);
-//   * 8 compute warps, per pair:
-//       first core  Z_1[s, q] = sum_i X_1[0,i,s] Y_1[0,i,q]  (Eq. 12's K = A_x^T A_y) on the FP32 pipe from
-//                   global (L2-resident) memory, written straight into the next step's B-fragment layout,
-//                   overlapping the first interior stage's arrival;
-//       interior    the two rank-16 GEMMs of a slice i on the tensor cores (3xTF32 mma.sync m16n8k8, every bound
-//                   a compile-time constant), slices spread over the warps, partials reduced through shared
-//                   memory in a fixed order into the next step's B fragments;
-//       last core   fused into the last interior step's reduction: each thread holds one entry Z_{N-1}[r, p] and
-//                   multiplies it by sum_i X_N[r,i,0] Y_N[p,i,0] (FP32, from L2), then a fixed-order block
-//                   reduction.
+//     (one copy per plane into padded planes), full/empty mbarriers;
+//   * boundary warp: the two rank-1 cores of each pair (1 KB per core and train for I = 16 -- as a ring stage
+//     they would occupy a whole stage for 1/16 of its data and leave the next pair's first interior stage issued
+//     one short step ahead of its use), one pair ahead, on the FP32 pipe from global memory:
+//       Z_1[s, q] = sum_i X_1[0,i,s] Y_1[0,i,q]   (Eq. 12's K = A_x^T A_y), in B-fragment slot order;
+//       D[r, p]   = sum_i X_N[r,i,0] Y_N[p,i,0],  so that  Z_N = sum_{r,p} Z_{N-1}[r,p] D[r,p];
+//   * 8 compute warps: per interior step the two rank-16 GEMMs of each slice i on the tensor cores (3xTF32
+//     mma.sync m16n8k8, ldmatrix for the Y operand, every bound a compile-time constant), slices spread over
+//     the warps, partials reduced through shared memory in a fixed order into the next step's B fragments; the
+//     last interior step's reduction is fused with the last core (multiply by D, fixed-order block reduction).
 // Every core byte is read from HBM exactly once; nothing is written but the result.  Needs N >= 3.
 #include "tc_common.cuh"
 #include "ttc_internal.h"
@@ -57,74 +53,105 @@ __device__ __forceinline__ R16Pair r16_pair(const InnerArgs& a, int k) {
     return p;
 }
 
-__device__ __forceinline__ void prefetch_l2(const float* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// Plane strides: X planes at = 8 mod 32 floats (conflict-free 8-byte B-fragment loads), Y planes at = 4 mod 8
+// floats (the 8 rows of an ldmatrix phase fall in 8 distinct 16-byte bank groups).
+__host__ __device__ __forceinline__ int ps_x(int floats) { return plane_stride(floats); }
+__host__ __device__ __forceinline__ int ps_y(int floats) {
+    int ps = (floats + 3) & ~3;
+    return (ps & 7) ? ps : ps + 4;
 }
 
-// Producer: stage interior core n (planes of 16 x I floats: plane v at v * ps, ps = 8 mod 32 so that fragment
-// loads are conflict-free), X planes then Y planes.
+// Producer: stage interior core n (planes of 16 x I floats at the strides above), X planes then Y planes.
 __device__ __forceinline__ void r16_issue(const float* xs, const float* ys, int I, float* stage, uint64_t* bar,
                                           const R16Layout& lay) {
     const int lane = threadIdx.x & 31;
     const int plane = 16 * I;
     if (lane == 0) mbar_arrive_expect_tx(bar, 4u * 2 * 16 * plane);
     __syncwarp();
-    const int ps = plane_stride(plane);
-    if (lane < 16) bulk_g2s(stage + lane * ps, xs + (int64_t)lane * plane, 4u * plane, bar);
-    else bulk_g2s(stage + lay.x_floats + (lane - 16) * ps, ys + (int64_t)(lane - 16) * plane, 4u * plane, bar);
+    if (lane < 16) bulk_g2s(stage + lane * ps_x(plane), xs + (int64_t)lane * plane, 4u * plane, bar);
+    else bulk_g2s(stage + lay.x_floats + (lane - 16) * ps_y(plane), ys + (int64_t)(lane - 16) * plane, 4u * plane, bar);
 }
 
-// One interior slice pair/single, identical arithmetic to inner_fast.cu's interior16.
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const float* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+// 3xTF32 parts of data read from shared memory: hi = the raw bits (the tensor core truncates to tf32),
+// lo = x - trunc(x) exactly.
+__device__ __forceinline__ uint32_t lo_trunc(uint32_t x) {
+    return __float_as_uint(__uint_as_float(x) - __uint_as_float(x & 0xffffe000u));
+}
+
+// U slices of one interior step (mode index i = ui[x]):
+//   GEMM-1  Wt[q, r] = sum_p Y[p, i, q] Z[r, p]:   A = Y_i (m = q: plane, k = p: contiguous) by ldmatrix in natural
+//           k order; B = Z from zfrag (b0 = Z[8ng + g, 8kf + t], b1 = Z[8ng + g, 8kf + t + 4]).
+//   GEMM-2  Zt'[q, s] += sum_r Wt[q, r] X[r, i, s]: A = GEMM-1's C fragments re-read as k-permuted A fragments
+//           (k slot t <-> r = 2t, slot t + 4 <-> r = 2t + 1: {c0, c2, c1, c3}); B = X_i with the same permutation,
+//           b0, b1 = X[8kb + 2t, i, 8ns + g], X[8kb + 2t + 1, i, 8ns + g]: one 8-byte load lands in fragment order.
+// yl: this lane's ldmatrix row address (row q = (lane & 7) + 8 ((lane >> 3) & 1), k offset 4 (lane >> 4)) at i = 0,
+// xl: this lane's X address (plane g, element 2t) at i = 0.
 template <int U>
-__device__ __forceinline__ void r16_units(const float* F, const float* G, int ps, const int (&ui)[U], int lg, int t,
+__device__ __forceinline__ void r16_units(const float* yl, const float* xl, int psx, const int (&ui)[U],
                                           const BFrag (&zb)[2][2], float (&acc)[2][4]) {
     float w[U][2][4];
 #pragma unroll
-    for (int x = 0; x < U; ++x) {   // GEMM-1: W^T[(i, q), r] = sum_p Y[p, i, q] Z[r, p]
-        const float* p1 = F + lg * ps + ui[x] * 16 + 2 * t;
-        const float* p2 = p1 + 8 * ps;
+    for (int x = 0; x < U; ++x) {
         AFrag A[2];
 #pragma unroll
         for (int kf = 0; kf < 2; ++kf) {
-            const float2 a1 = *reinterpret_cast<const float2*>(p1 + 8 * kf);
-            const float2 a2 = *reinterpret_cast<const float2*>(p2 + 8 * kf);
-            const float fa[4] = {a1.x, a2.x, a1.y, a2.y};
-            A[kf] = split_a_trunc(fa);
+            ldsm_x4(A[kf].hi, yl + ui[x] * 16 + 8 * kf);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) A[kf].lo[c] = lo_trunc(A[kf].hi[c]);
         }
 #pragma unroll
         for (int ng = 0; ng < 2; ++ng) mma6<true>(w[x][ng], A[0], zb[0][ng], A[1], zb[1][ng]);
     }
 #pragma unroll
-    for (int x = 0; x < U; ++x) {   // GEMM-2: Z'[s, q] += sum_r X[r, i, s] W[r, i, q]
-        const float* p1 = G + lg * ps + ui[x] * 16 + 2 * t;
-        const float* p2 = p1 + 8 * ps;
-        AFrag A[2];
+    for (int x = 0; x < U; ++x) {
+        AFrag Aw[2];
 #pragma unroll
-        for (int kg = 0; kg < 2; ++kg) {
-            const float2 a1 = *reinterpret_cast<const float2*>(p1 + 8 * kg);
-            const float2 a2 = *reinterpret_cast<const float2*>(p2 + 8 * kg);
-            const float ga[4] = {a1.x, a2.x, a1.y, a2.y};
-            A[kg] = split_a_trunc(ga);
+        for (int kb = 0; kb < 2; ++kb) {
+            const float c4[4] = {w[x][kb][0], w[x][kb][2], w[x][kb][1], w[x][kb][3]};
+            Aw[kb] = split_a(c4);
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const BFrag B0 = split_b(w[x][0][2 * h], w[x][0][2 * h + 1]);
-            const BFrag B1 = split_b(w[x][1][2 * h], w[x][1][2 * h + 1]);
-            float tg[4];
-            mma6<true>(tg, A[0], B0, A[1], B1);
+        for (int ns = 0; ns < 2; ++ns) {
+            BFrag B[2];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[h][c] += tg[c];
+            for (int kb = 0; kb < 2; ++kb) {
+                const uint2 v = *reinterpret_cast<const uint2*>(xl + 8 * ns * psx + ui[x] * 16 + 8 * kb);
+                B[kb].hi[0] = v.x;
+                B[kb].hi[1] = v.y;
+                B[kb].lo[0] = lo_trunc(v.x);
+                B[kb].lo[1] = lo_trunc(v.y);
+            }
+            float tg[4];
+            mma6<true>(tg, Aw[0], B[0], Aw[1], B[1]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[ns][c] += tg[c];
         }
     }
+}
+
+// zfrag slot e = [kf][ng][ln][jj] holds Z[zg, zf] = Z[8 ng + ln/4, 8 kf + ln%4 + 4 jj] (zg on X's bond, zf on Y's):
+// the B fragments of the next GEMM-1 (b0 = Z[8ng + g, 8kf + t], b1 = Z[8ng + g, 8kf + t + 4]).
+__device__ __forceinline__ void slot_entry(int e, int& zg, int& zf) {
+    const int jj = e & 1, ln = (e >> 1) & 31, ng = (e >> 6) & 1, kf = e >> 7;
+    zg = 8 * ng + (ln >> 2);
+    zf = 8 * kf + (ln & 3) + 4 * jj;
 }
 
 __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Layout lay) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    __shared__ __align__(8) uint64_t z1full, z1empty, dfull, dempty;
     __shared__ float red[kCW];
     float* stages = smem;
     float* zpart = smem + kStages * lay.stage_floats;   // [kCW][2 n-tiles][32 lanes][4]
-    float* zfrag = zpart + kCW * kPart;           // [kf][ng][32 lanes][2]: B fragments of Z for the next step
+    float* zfrag = zpart + kCW * kPart;           // [slot]: B fragments of Z for the next step
+    float* z1buf = zfrag + kCT;                   // [slot]: Z_1 of the next pair (boundary warp)
+    float* dbuf = z1buf + kCT;                    // [slot]: sum_i X_N[zg,i,0] Y_N[zf,i,0] of the next pair
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int N = a.N, I0 = a.dims[0], IL = a.dims[N - 1];
 
@@ -133,6 +160,10 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
             mbar_init(&full[k], 1);
             mbar_init(&empty[k], kCW);
         }
+        mbar_init(&z1full, 32);
+        mbar_init(&dfull, 32);
+        mbar_init(&z1empty, 1);
+        mbar_init(&dempty, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -144,9 +175,6 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
             if (!p.valid) break;
             const float* xs = a.x.cores + p.xo;
             const float* ys = a.y.cores + p.yo;
-            // boundary cores -> L2 (the compute warps read them with plain loads)
-            if (lane == 0) prefetch_l2(xs, 4u * 16 * I0);
-            if (lane == 1) prefetch_l2(ys, 4u * 16 * I0);
             int64_t off = 16 * (int64_t)I0;
             for (int n = 1; n < N - 1; ++n, ++j) {
                 const int st = j % kStages;
@@ -155,59 +183,83 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
                 r16_issue(xs + off, ys + off, I, stages + st * lay.stage_floats, &full[st], lay);
                 off += 256 * (int64_t)I;
             }
-            if (lane == 0) prefetch_l2(xs + off, 4u * 16 * IL);
-            if (lane == 1) prefetch_l2(ys + off, 4u * 16 * IL);
+        }
+        return;
+    }
+    if (warp == kCW + 1) {   // ------------------------------------------------------------- boundary warp
+        // The two rank-1 cores of each pair on the FP32 pipe, one pair ahead of the compute warps, from global
+        // memory (1 KB per core and train for I = 16: a TMA stage would be 1/16 full):
+        //   Z_1[s, q] = sum_i X_1[0,i,s] Y_1[0,i,q]  (Eq. 12's K = A_x^T A_y)          -> z1buf
+        //   D[r, p]   = sum_i X_N[r,i,0] Y_N[p,i,0]  (so that Z_N = sum_{r,p} Z_{N-1}[r,p] D[r,p])  -> dbuf
+        int64_t last = 16 * (int64_t)I0;
+        for (int n = 1; n < N - 1; ++n) last += 256 * (int64_t)a.dims[n];
+        for (int k = 0;; ++k) {
+            const R16Pair p = r16_pair(a, k);
+            if (!p.valid) break;
+            const float* xs = a.x.cores + p.xo;
+            const float* ys = a.y.cores + p.yo;
+            if (k > 0) mbar_wait(&z1empty, (k - 1) & 1);
+            for (int e = lane; e < kCT; e += 32) {
+                int zg, zf;
+                slot_entry(e, zg, zf);
+                const float* xr = xs + I0 * zg;
+                const float* yr = ys + I0 * zf;
+                float d = 0.f;
+                if ((I0 & 3) == 0) {
+                    for (int i = 0; i < I0; i += 4) {
+                        const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + i));
+                        const float4 yv = __ldg(reinterpret_cast<const float4*>(yr + i));
+                        d = fmaf(xv.x, yv.x, d);
+                        d = fmaf(xv.y, yv.y, d);
+                        d = fmaf(xv.z, yv.z, d);
+                        d = fmaf(xv.w, yv.w, d);
+                    }
+                } else {
+                    for (int i = 0; i < I0; ++i) d = fmaf(__ldg(xr + i), __ldg(yr + i), d);
+                }
+                z1buf[e] = d;
+            }
+            mbar_arrive(&z1full);
+            if (k > 0) mbar_wait(&dempty, (k - 1) & 1);
+            const float* xl = xs + last;
+            const float* yl = ys + last;
+            for (int e = lane; e < kCT; e += 32) {
+                int zg, zf;
+                slot_entry(e, zg, zf);
+                float d = 0.f;
+                for (int i = 0; i < IL; ++i) d = fmaf(__ldg(xl + zg + 16 * i), __ldg(yl + zf + 16 * i), d);
+                dbuf[e] = d;
+            }
+            mbar_arrive(&dfull);
         }
         return;
     }
 
     // ------------------------------------------------------------------------------------------ compute
     const int tid = threadIdx.x, lg = lane >> 2, t = lane & 3;
-    // this thread's zfrag slot e = tid: Z entry (g, f) = (8 ng + ln/4, 8 kf + 2 (ln%4) + jj) and its source in a
-    // warp's fragment-native partial Z' (C fragment of n-tile nf = f / 8: lane 4 (g%8) + (f%8)/2, element
-    // 2 (g/8) + f%2)
-    const int e_jj = tid & 1, e_ln = (tid >> 1) & 31, e_ng = (tid >> 6) & 1, e_kf = tid >> 7;
-    const int zg = 8 * e_ng + (e_ln >> 2), zf = 8 * e_kf + 2 * (e_ln & 3) + e_jj;
-    const int src = ((zf >> 3) * 32 + ((zg & 7) << 2) + ((zf & 7) >> 1)) * 4 + ((zg >> 3) << 1) + (zf & 1);
+    // this thread's zfrag slot is tid; its source in a warp's fragment-native partial Zt'[q = zf, s = zg] is the
+    // C fragment of n-tile zg / 8: lane 4 (zf % 8) + (zg % 8) / 2, element 2 (zf / 8) + zg % 2
+    int zg, zf;
+    slot_entry(tid, zg, zf);
+    const int src = ((zg >> 3) * 32 + ((zf & 7) << 2) + ((zg & 7) >> 1)) * 4 + ((zf >> 3) << 1) + (zg & 1);
+    const int yrow = (lane & 7) + 8 * ((lane >> 3) & 1), ykoff = 4 * (lane >> 4);
 
     int j = 0;
     for (int k = 0;; ++k) {
         const R16Pair p = r16_pair(a, k);
         if (!p.valid) break;
-        const float* xs = a.x.cores + p.xo;
-        const float* ys = a.y.cores + p.yo;
-        {   // ---- first core: Z_1[s, q] = sum_i X_1[0,i,s] Y_1[0,i,q] (= A_x^T A_y, Eq. 12) into slot tid.
-            // Safe to overwrite zfrag: every warp passed the previous pair's partials barrier, after its last read.
-            const float* xr = xs + I0 * zg;
-            const float* yr = ys + I0 * zf;
-            float d = 0.f;
-            if ((I0 & 3) == 0) {
-                for (int i = 0; i < I0; i += 4) {
-                    const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + i));
-                    const float4 yv = __ldg(reinterpret_cast<const float4*>(yr + i));
-                    d = fmaf(xv.x, yv.x, d);
-                    d = fmaf(xv.y, yv.y, d);
-                    d = fmaf(xv.z, yv.z, d);
-                    d = fmaf(xv.w, yv.w, d);
-                }
-            } else {
-                for (int i = 0; i < I0; ++i) d = fmaf(__ldg(xr + i), __ldg(yr + i), d);
-            }
-            zfrag[tid] = d;
-            bar_named(1, kCT);
-        }
-        int64_t off = 16 * (int64_t)I0;
+        mbar_wait(&z1full, k & 1);   // Z_1 of this pair in z1buf
         for (int n = 1; n < N - 1; ++n, ++j) {
             const int st = j % kStages;
             const int I = a.dims[n];
-            off += 256 * (int64_t)I;
             // ---- interior step
+            const float* zsrc = n == 1 ? z1buf : zfrag;
             BFrag zb[2][2];
 #pragma unroll
             for (int kf = 0; kf < 2; ++kf)
 #pragma unroll
                 for (int ng = 0; ng < 2; ++ng) {
-                    const float2 v2 = *reinterpret_cast<const float2*>(zfrag + ((kf * 2 + ng) * 32 + lane) * 2);
+                    const float2 v2 = *reinterpret_cast<const float2*>(zsrc + ((kf * 2 + ng) * 32 + lane) * 2);
                     zb[kf][ng] = split_b(v2.x, v2.y);
                 }
             float acc[2][4];
@@ -218,15 +270,17 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
             mbar_wait(&full[st], (j / kStages) & 1);
             const float* X = stages + st * lay.stage_floats;
             const float* Y = X + lay.x_floats;
-            const int ps = plane_stride(16 * I);
+            const int psx = ps_x(16 * I);
+            const float* yl = Y + yrow * ps_y(16 * I) + ykoff;
+            const float* xl = X + lg * psx + 2 * t;
             int i = warp;
             for (; i + kCW < I; i += 2 * kCW) {
                 const int uu[2] = {i, i + kCW};
-                r16_units<2>(Y, X, ps, uu, lg, t, zb, acc);
+                r16_units<2>(yl, xl, psx, uu, zb, acc);
             }
             if (i < I) {
                 const int uu[1] = {i};
-                r16_units<1>(Y, X, ps, uu, lg, t, zb, acc);
+                r16_units<1>(yl, xl, psx, uu, zb, acc);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
@@ -234,30 +288,24 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
 #pragma unroll
             for (int h = 0; h < 2; ++h)
                 *reinterpret_cast<float4*>(zw + (h * 32 + lane) * 4) = make_float4(acc[h][0], acc[h][1], acc[h][2], acc[h][3]);
-            if (n < N - 2) {
-                bar_named(1, kCT);   // partials visible
-                float v = 0.f;
+            bar_named(1, kCT);   // partials visible; every warp is done with zfrag / z1buf
+            if (n == 1 && tid == 0) mbar_arrive(&z1empty);
+            float v = 0.f;
 #pragma unroll
-                for (int w = 0; w < kCW; ++w) v += zpart[w * kPart + src];
+            for (int w = 0; w < kCW; ++w) v += zpart[w * kPart + src];
+            if (n < N - 2) {
                 zfrag[tid] = v;
                 bar_named(1, kCT);   // next step's B fragments visible; partials free
             } else {
-                // ---- last core fused: Z_N = sum_{r,p} Z_{N-1}[r,p] sum_i X_N[r,i,0] Y_N[p,i,0]; this thread owns
-                // Z_{N-1}[zg, zf].  The L2 loads are issued before the barrier.
-                const float* xl = xs + off;
-                const float* yl = ys + off;
-                float d = 0.f;
-                for (int i2 = 0; i2 < IL; ++i2) d = fmaf(__ldg(xl + zg + 16 * i2), __ldg(yl + zf + 16 * i2), d);
-                bar_named(1, kCT);   // partials visible
-                float v = 0.f;
-#pragma unroll
-                for (int w = 0; w < kCW; ++w) v += zpart[w * kPart + src];
-                v *= d;
+                // ---- last core: Z_N = sum_{r,p} Z_{N-1}[r,p] D[r,p]; this thread owns Z_{N-1}[zg, zf]
+                mbar_wait(&dfull, k & 1);
+                v *= dbuf[tid];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 if (lane == 0) red[warp] = v;
-                bar_named(1, kCT);   // red visible; partials free
+                bar_named(1, kCT);   // red visible; partials and dbuf free
                 if (tid == 0) {
+                    mbar_arrive(&dempty);
                     float s = 0.f;
 #pragma unroll
                     for (int w = 0; w < kCW; ++w) s += red[w];
@@ -275,7 +323,7 @@ bool inner_r16_supported(const InnerArgs& a, bool uniform_r16) {
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
     // two stages of 2 x 16 padded planes + partials + fragments
-    const size_t smem = sizeof(float) * (kStages * (size_t)2 * 16 * plane_stride(16 * max_dim) + kCW * kPart + kCT);
+    const size_t smem = sizeof(float) * (kStages * (size_t)16 * (ps_x(16 * max_dim) + ps_y(16 * max_dim)) + kCW * kPart + 3 * kCT);
     return smem <= 112 * 1024;   // two CTAs per SM
 }
 
@@ -283,20 +331,20 @@ cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s) {
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
     R16Layout lay;
-    lay.ps_max = plane_stride(16 * max_dim);
+    lay.ps_max = ps_x(16 * max_dim);
     lay.x_floats = 16 * lay.ps_max;
-    lay.stage_floats = 2 * lay.x_floats;
-    const size_t smem = sizeof(float) * (kStages * (size_t)lay.stage_floats + kCW * kPart + kCT);
+    lay.stage_floats = lay.x_floats + 16 * ps_y(16 * max_dim);
+    const size_t smem = sizeof(float) * (kStages * (size_t)lay.stage_floats + kCW * kPart + 3 * kCT);
     cudaError_t e = cudaFuncSetAttribute(inner_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_r16_kernel, 32 * (kCW + 1), smem)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_r16_kernel, 32 * (kCW + 2), smem)) != cudaSuccess)
         return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int grid = a.B < sms * per_sm ? a.B : sms * per_sm;
-    inner_r16_kernel<<<grid, 32 * (kCW + 1), smem, s>>>(a, lay);
+    inner_r16_kernel<<<grid, 32 * (kCW + 2), smem, s>>>(a, lay);
     return cudaGetLastError();
 }
 
