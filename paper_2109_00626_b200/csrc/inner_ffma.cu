@@ -1,0 +1,431 @@
+// inner_ffma.cu -- tt_inner, one warp per pair on the FP32 pipe, for interior bond ranks that are multiples of 8
+// and <= 32 (BASELINE.json C5: N = 64, I = 2, ranks drawn from {8, 16, 24, 32} per bond).  Same sweep as ttc.h:
+//   Z_0 = [1],  Z_n = sum_i X_n[:, i, :]^T Z_{n-1} Y_n[:, i, :]   (Fig. 1b / Eq. 12 chained),  out = Z_N.
+//
+// Why FP32 and not the tensor cores here: C5's steps are tiny (8..32-wide) and rectangular, so 16-row mma
+// tiles pad 20% of the work away and 3xTF32 triples the rest; measured legacy mma.sync tf32 (279 TF) then
+// caps the sweep near 10 M pairs/s, while FFMA at 72 TF caps it near 23 M pairs/s.
+//
+// Per step, with the cheaper association (F = the core multiplied into Z first, G = the other one):
+//   GEMM-1 (per slice i):  W_i[g, f'] = sum_f Z[g, f] F[f, i, f']          (Ga x Fb, K = Fa)
+//   GEMM-2 (per slice i):  Z'[g', f'] += sum_g G[g, i, g'] W_i[g, f']      (Gb x Fb, K = Ga)
+// W-first: F = Y, G = X (Z indexed [x bond][y bond]); V-first: F = X, G = Y (Z stored transposed).
+// Every operand is read along its contraction index, which is the contiguous one in the paper's core
+// layout (Eq. 2), so each lane loads 4 K-values with one 16-byte LDS and does 4 FFMA per output it owns.
+// Lane (lg = lane / 4, lf = lane % 4) owns rows lg + 8a and columns lf + 4b of each output tile.
+//
+// Staging: the warp copies its own future steps into a private ring with 16-byte cp.async, inserting 4 floats
+// of padding after every contiguous run (F: runs of Fa, G: runs of Ga*I) so that the 8 (or 4) distinct runs
+// one LDS.128 touches fall into distinct bank groups; Z and W are kept with padded row strides likewise.
+// Pairs are handed out by a per-launch atomic ticket (dynamic load balance over heterogeneous pairs).
+#include <algorithm>
+#include <atomic>
+
+#include "tc_common.cuh"
+#include "ttc_internal.h"
+
+namespace ttc {
+namespace {
+
+constexpr int kPad = 4;
+constexpr int kQ = 4;                   // staged steps in flight per warp
+constexpr int kSlots = 1024;            // ticket counters (one per launch, reused round robin)
+
+constexpr int kMagicMax = 1024;          // exact-division table: q in [2, kMagicMax]
+
+// c_magic[q] = ceil(2^32 / q): e / q == __umulhi(e, c_magic[q]) for every e < 2^32 / q (q >= 2).
+struct MagicTable {
+    unsigned v[kMagicMax + 1];
+    constexpr MagicTable() : v() {
+        for (int q = 2; q <= kMagicMax; ++q) v[q] = (unsigned)((0x100000000ull + q - 1) / q);
+    }
+};
+__constant__ MagicTable c_magic = MagicTable();
+
+__device__ unsigned int g_ticket[kSlots];
+__device__ unsigned int g_done[kSlots];
+
+struct FfArgs {
+    int ring;         // floats of one warp's ring
+    int zbuf, wbuf;   // floats of the Z and W buffers
+    int warp_floats;  // ring + Z + W + queue
+    int slot;         // ticket counter of this launch
+};
+
+struct FStep {
+    int start;        // ring offset (floats) of the F region (boundary steps: X), G (Y) follows
+    int b, n, R, P, S, Q, I;
+    int vf;           // interior: V-first (F = X); boundary: unused
+    int znext;        // orientation the next step wants Z in (1: transposed, V-first next)
+    unsigned end;     // monotone ring position after this step
+};
+
+__device__ __forceinline__ int frank(const TrainDev& t, int b, int N, int n) {
+    if (n <= 0 || n >= N) return 1;
+    return t.ranks ? __ldg(t.ranks + (int64_t)b * (N + 1) + n) : t.urank;
+}
+__device__ __forceinline__ int64_t fbase(const TrainDev& t, int b) {
+    return t.offsets ? __ldg(t.offsets + b) : (int64_t)b * t.train_elems;
+}
+// V-first (X multiplied into Z first) iff it is strictly cheaper: I S P (R + Q) < I R Q (P + S)
+__device__ __forceinline__ int vfirst(int R, int P, int S, int Q) { return S * P * (R + Q) < R * Q * (P + S); }
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// Packed FP32 pair (FFMA2 on sm_100a: two FMAs per issue slot at the same FP32 throughput, measured
+// tools/fma_bench.cu).  acc.{x,y} accumulate the even / odd k terms of a dot product.
+__device__ __forceinline__ unsigned long long pk(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void fma2(unsigned long long& acc, unsigned long long a, unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float hsum2(unsigned long long v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return lo + hi;
+}
+// acc += a.xy * b.xy, a.zw * b.zw (pairwise): the 4-term dot product in two FFMA2
+__device__ __forceinline__ void dot4x2(unsigned long long& acc, const float4 a, const float4 b) {
+    fma2(acc, pk(a.x, a.y), pk(b.x, b.y));
+    fma2(acc, pk(a.z, a.w), pk(b.z, b.w));
+}
+__device__ __forceinline__ float dot4(float acc, const float4 a, const float4 b) {
+    acc = fmaf(a.x, b.x, acc);
+    acc = fmaf(a.y, b.y, acc);
+    acc = fmaf(a.z, b.z, acc);
+    return fmaf(a.w, b.w, acc);
+}
+
+// Copy `runs` runs of `run` floats (run % 4 == 0) from contiguous global memory into shared memory with a run
+// stride of run + kPad (run / 4 in [2, kMagicMax]): e / (run / 4) is one IMAD.HI with the magic table.
+__device__ __forceinline__ void stage_padded(float* dst, const float* src, int runs, int run, int lane) {
+    const unsigned q = (unsigned)run >> 2;
+    const unsigned div = c_magic.v[q];
+    const unsigned chunks = (unsigned)runs * q;
+    for (unsigned e = lane; e < chunks; e += 32) {
+        const unsigned c = __umulhi(e, div);
+        const unsigned o = e - c * q;
+        tc::cp_async16(dst + c * (run + kPad) + 4 * o, src + 4 * e);
+    }
+}
+__device__ __forceinline__ void stage_plain(float* dst, const float* src, int n, int lane) {
+    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+        for (int e = 4 * lane; e < n; e += 128) tc::cp_async16(dst + e, src + e);
+    } else {   // odd boundary sizes (N = 1, I odd): plain copies, visible after the consumer's __syncwarp
+        for (int e = lane; e < n; e += 32) dst[e] = __ldg(src + e);
+    }
+}
+
+// Register-tiled block product and store: for rows lg + 8a (a < TA) and columns c0 + lf + 4b (b < NB),
+//   out[row * rs + col * cs + (col / I) * ci] = sum_k A[row][k] B[col][k]
+// A rows and B columns are contiguous along k (strides sA / sB, 16-byte aligned).  The (col / I) term inserts
+// the W buffer's column padding (ci = 0: none).  The next k-chunk's operands are loaded before the current
+// chunk's FFMAs issue (software pipelining: LDS latency hides behind 4 TA NB FFMAs).  Only the 8
+// instantiations below exist, inside one non-inlined ff_gemm, for every shape and both GEMMs: the hot code
+// stays inside the SM's instruction caches (~6 KB L0, 32 KB L1.5) although every warp runs another shape.
+template <int TA, int NB>
+__device__ __forceinline__ void block_fma(const float* __restrict__ A, int sA, const float* __restrict__ B, int sB, int K,
+                                          float* __restrict__ out, int rs, int cs, int ci, unsigned idiv, int c0,
+                                          int lg, int lf) {
+    unsigned long long acc[TA][NB];
+#pragma unroll
+    for (int a = 0; a < TA; ++a)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) acc[a][b] = 0ull;
+    const float* Ap[TA];
+    const float* Bp[NB];
+#pragma unroll
+    for (int a = 0; a < TA; ++a) Ap[a] = A + 8 * a * sA;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) Bp[b] = B + (c0 + lf + 4 * b) * sB;
+    float4 za[TA], fb[NB];
+#pragma unroll
+    for (int a = 0; a < TA; ++a) za[a] = ld4(Ap[a]);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) fb[b] = ld4(Bp[b]);
+#pragma unroll 2
+    for (int k = 4; k <= K; k += 4) {
+        float4 zn[TA], fn[NB];
+        const int kk = k < K ? k : 0;   // the last iteration re-reads chunk 0 (in bounds, discarded)
+#pragma unroll
+        for (int a = 0; a < TA; ++a) zn[a] = ld4(Ap[a] + kk);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) fn[b] = ld4(Bp[b] + kk);
+#pragma unroll
+        for (int a = 0; a < TA; ++a)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) dot4x2(acc[a][b], za[a], fb[b]);
+#pragma unroll
+        for (int a = 0; a < TA; ++a) za[a] = zn[a];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) fb[b] = fn[b];
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const unsigned col = c0 + lf + 4 * b;
+        const int cbase = col * cs + (ci ? (int)__umulhi(col, idiv) * ci : 0);
+#pragma unroll
+        for (int a = 0; a < TA; ++a) out[(lg + 8 * a) * rs + cbase] = hsum2(acc[a][b]);
+    }
+}
+
+// out = A B^T over rows < 8 TA and columns < 4 ncols (ncols even), in blocks of 4 columns per lane.
+__device__ __noinline__ void ff_gemm(const float* A, int sA, const float* B, int sB, int K, int TA, int ncols,
+                                     float* out, int rs, int cs, int ci, unsigned idiv, int lane) {
+    const int lg = lane >> 2, lf = lane & 3;
+    A += lg * sA;
+    for (int cb = 0; cb < ncols; cb += 4) {
+        const int c0 = 4 * cb;
+#define FF_CASE(ta, nb) \
+    case 2 * (ta) + (nb) / 4 - 1: block_fma<ta, nb>(A, sA, B, sB, K, out, rs, cs, ci, idiv, c0, lg, lf); break;
+        switch (2 * TA + (ncols - cb >= 4 ? 1 : 0) - 1) {
+            FF_CASE(1, 2) FF_CASE(1, 4) FF_CASE(2, 2) FF_CASE(2, 4)
+            FF_CASE(3, 2) FF_CASE(3, 4) FF_CASE(4, 2) FF_CASE(4, 4)
+            default: break;
+        }
+#undef FF_CASE
+    }
+}
+
+// One interior step.  Z: [g][f] with row stride Fa + kPad.  GEMM-1 writes W[g + Ga c + kPad (c / I)] for F
+// column c = i + I f' (so that GEMM-2 reads W column f' as one contiguous run over (g, i)); GEMM-2 writes Z'
+// in the orientation the next step reads: same (flip = 0): [g'][f'] stride Fb + kPad; flip: [f'][g'] stride
+// Gb + kPad.
+__device__ __forceinline__ void ff_step(const float* F, int Fa, int Fb, const float* G, int Ga, int Gb, int I, float* Z,
+                                        float* W, int flip, int lane) {
+    const unsigned idiv = I == 1 ? 0u : c_magic.v[I];
+    const int sF = Fa + kPad, sG = Ga * I + kPad;
+    // GEMM-1: W[g, c] = sum_f Z[g, f] F[f, c]     (Ga x I Fb, K = Fa)
+    ff_gemm(Z, sF, F, sF, Fa, Ga >> 3, (I * Fb) >> 2, W, 1, I == 1 ? Ga + kPad : Ga, I == 1 ? 0 : kPad, idiv, lane);
+    __syncwarp();
+    // GEMM-2: Z'[g', f'] = sum_(g,i) G[(g,i), g'] W[(g,i), f']   (Gb x Fb, K = Ga I)
+    const int sW = Ga * I + kPad;
+    ff_gemm(G, sG, W, sW, Ga * I, Gb >> 3, Fb >> 2, Z, flip ? 1 : Fb + kPad, flip ? Gb + kPad : 1, 0, 0u, lane);
+    __syncwarp();
+}
+
+// First step (R = P = 1): Z_1[s, q] = sum_i X_1[0, i, s] Y_1[0, i, q] -- Eq. 12's K -- stored for the next step:
+// znext = 0: Z[s][q] stride Q + kPad, znext = 1: Z[q][s] stride S + kPad.
+__device__ __forceinline__ void ff_first(const float* X, const float* Y, int S, int Q, int I, int znext, float* Z,
+                                         int lane) {
+    for (int q = 0; q < Q; ++q)
+        for (int s = lane; s < S; s += 32) {
+            float d = 0.f;
+            for (int i = 0; i < I; ++i) d = fmaf(X[i + I * s], Y[i + I * q], d);
+            Z[znext ? q * (S + kPad) + s : s * (Q + kPad) + q] = d;
+        }
+    __syncwarp();
+}
+// Last step (S = Q = 1): Z_N = sum_{r,p} Z[r,p] sum_i X_N[r,i,0] Y_N[p,i,0], Z[r][p] stride P + kPad (first:
+// N = 1, Z_0 = 1).  Warp-reduced in a fixed order.
+__device__ __forceinline__ float ff_last(const float* X, const float* Y, int R, int P, int I, bool first, const float* Z,
+                                         int lane) {
+    float v = 0.f;
+    for (int p = 0; p < P; ++p)
+        for (int r = lane; r < R; r += 32) {
+            float d = 0.f;
+            for (int i = 0; i < I; ++i) d = fmaf(X[r + R * i], Y[p + P * i], d);
+            v = fmaf(first ? 1.0f : Z[r * (P + kPad) + p], d, v);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+struct FCursor {
+    int b, n, R, P;
+    int64_t xo, yo;
+    bool valid;
+};
+
+// Next pair from the launch's ticket counter; its rank rows go to rk (X: rk[0..N], Y: rk[N+1..2N+1]).
+__device__ __forceinline__ void fc_pop(const InnerArgs& a, const FfArgs& w, FCursor& c, int* rk, int lane) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&g_ticket[w.slot], 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    c.valid = t < (unsigned)a.B;
+    if (!c.valid) return;
+    c.b = a.order ? __ldg(a.order + t) : (int)t;
+    const int N = a.N;
+    __syncwarp();   // every lane is done reading the previous pair's ranks
+    for (int n = lane; n <= N; n += 32) {
+        rk[n] = frank(a.x, c.b, N, n);
+        rk[N + 1 + n] = frank(a.y, c.b, N, n);
+    }
+    __syncwarp();
+    c.n = 0;
+    c.R = 1;
+    c.P = 1;
+    c.xo = fbase(a.x, c.b);
+    c.yo = fbase(a.y, c.b);
+}
+
+// One warp per CTA (warps never synchronise with each other); several CTAs per SM, as shared memory allows.
+__global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const FfArgs w) {
+    extern __shared__ __align__(16) float smem[];
+    const int lane = threadIdx.x & 31;
+    float* ring = smem;
+    float* Z = ring + w.ring;
+    float* W = Z + w.zbuf;
+    FStep* q = reinterpret_cast<FStep*>(W + w.wbuf);
+    int* rk = reinterpret_cast<int*>(q + kQ);
+    const int N = a.N;
+    FCursor ic;
+    fc_pop(a, w, ic, rk, lane);
+    unsigned head = 0, tail = 0, head_off = 0;
+    int qh = 0, qn = 0;
+    const unsigned RING = (unsigned)w.ring;
+    while (true) {
+        // ---- stage future steps while they fit
+        while (ic.valid && qn < kQ) {
+            const int n = ic.n, I = a.dims[n];
+            const int R = ic.R, P = ic.P;
+            const int S = rk[n + 1], Q = rk[N + 2 + n];
+            const bool boundary = n == 0 || n == N - 1;
+            int vf = 0, need;
+            if (boundary) {
+                need = ((R * I * S + 3) & ~3) + ((P * I * Q + 3) & ~3);
+            } else {
+                vf = vfirst(R, P, S, Q);
+                const int Fa = vf ? R : P, Fb = vf ? S : Q, Ga = vf ? P : R, Gb = vf ? Q : S;
+                need = I * Fb * (Fa + kPad) + Gb * (Ga * I + kPad);
+            }
+            unsigned start = head, start_off = head_off;
+            if (start_off + need > RING) { start += RING - start_off; start_off = 0; }   // never wrap a step
+            if (qn == 0) tail = start;
+            if (start + need - tail > RING) break;                                      // no room yet
+            float* dst = ring + start_off;
+            const float* xs = a.x.cores + ic.xo;
+            const float* ys = a.y.cores + ic.yo;
+            if (boundary) {
+                stage_plain(dst, xs, R * I * S, lane);
+                stage_plain(dst + ((R * I * S + 3) & ~3), ys, P * I * Q, lane);
+            } else {
+                const float* Fs = vf ? xs : ys;
+                const float* Gs = vf ? ys : xs;
+                const int Fa = vf ? R : P, Fb = vf ? S : Q, Ga = vf ? P : R, Gb = vf ? Q : S;
+                stage_padded(dst, Fs, I * Fb, Fa, lane);
+                stage_padded(dst + I * Fb * (Fa + kPad), Gs, Gb, Ga * I, lane);
+            }
+            tc::cp_commit_group();
+            int znext = 0;   // the next step's Z orientation (the last step reads [r][p])
+            if (n + 1 < N - 1) znext = vfirst(S, Q, rk[n + 2], rk[N + 3 + n]);
+            if (lane == 0) {
+                FStep f;
+                f.start = (int)start_off;
+                f.b = ic.b; f.n = n; f.R = R; f.P = P; f.S = S; f.Q = Q; f.I = I;
+                f.vf = vf;
+                f.znext = znext;
+                f.end = start + need;
+                q[(qh + qn) % kQ] = f;
+            }
+            ++qn;
+            head = start + need;
+            head_off = start_off + need;
+            ic.xo += (int64_t)R * I * S;
+            ic.yo += (int64_t)P * I * Q;
+            ic.R = S;
+            ic.P = Q;
+            if (++ic.n == N) fc_pop(a, w, ic, rk, lane);
+        }
+        if (qn == 0) break;
+        // ---- compute the oldest staged step
+        tc::cp_wait_pending(qn - 1);
+        __syncwarp();
+        const FStep f = q[qh];
+        float* X = ring + f.start;
+        if (f.n == N - 1) {   // last step (also N = 1)
+            const float* Y = X + ((f.R * f.I * f.S + 3) & ~3);
+            const float v = ff_last(X, Y, f.R, f.P, f.I, f.n == 0, Z, lane);
+            if (lane == 0) a.out[f.b] = v;
+        } else if (f.n == 0) {
+            const float* Y = X + ((f.R * f.I * f.S + 3) & ~3);
+            ff_first(X, Y, f.S, f.Q, f.I, f.znext, Z, lane);
+        } else {
+            const int vf = f.vf;
+            const int Fa = vf ? f.R : f.P, Fb = vf ? f.S : f.Q, Ga = vf ? f.P : f.R, Gb = vf ? f.Q : f.S;
+            const float* G = X + f.I * Fb * (Fa + kPad);
+            ff_step(X, Fa, Fb, G, Ga, Gb, f.I, Z, W, f.znext != vf, lane);
+        }
+        __syncwarp();
+        tail = f.end;
+        qh = (qh + 1) % kQ;
+        --qn;
+    }
+    tc::cp_wait_pending(0);
+    // the last warp of the launch resets its ticket slot for a later launch
+    if (lane == 0) {
+        __threadfence();
+        const unsigned total = gridDim.x;
+        if (atomicAdd(&g_done[w.slot], 1u) == total - 1) {
+            g_ticket[w.slot] = 0;
+            g_done[w.slot] = 0;
+            __threadfence();
+        }
+    }
+}
+
+// Floats of the per-warp buffers for a batch whose interior ranks are <= max_rank and dims <= max_dim.
+struct FfSizes {
+    int64_t step, zbuf, wbuf, qf;   // qf: step queue + the staged pair's rank rows
+};
+FfSizes ffma_sizes(int max_rank, int max_dim, int N) {
+    const int64_t r = max_rank, I = max_dim;
+    FfSizes z;
+    z.step = I * r * (r + kPad) + r * (r * I + kPad) + 64;   // padded F + G regions of the largest step (+ slack)
+    z.zbuf = r * (r + kPad);
+    z.wbuf = r * (r * I + kPad);
+    z.qf = (kQ * (int64_t)sizeof(FStep) / 4 + 2 * (N + 1) + 3) & ~int64_t(3);
+    return z;
+}
+constexpr int64_t kSmemPerSM = 228 * 1024, kSmemPerCTA = 227 * 1024, kReservedPerCTA = 1024;
+
+std::atomic<unsigned> g_launches{0};
+
+}  // namespace
+
+bool inner_ffma_supported(const InnerArgs& a, int max_rank, bool ranks_mult8) {
+    if (!ranks_mult8 || max_rank > 32 || a.N < 1) return false;
+    int max_dim = 1;
+    for (int n = 0; n < a.N; ++n) max_dim = std::max(max_dim, (int)a.dims[n]);
+    if (max_rank * max_dim / 4 > kMagicMax) return false;
+    const FfSizes z = ffma_sizes(max_rank, max_dim, a.N);
+    // at least 4 warps per SM, each holding one step of the largest shape
+    return 4 * (4 * (z.step + z.zbuf + z.wbuf + z.qf) + kReservedPerCTA) <= kSmemPerSM;
+}
+
+cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s) {
+    int max_dim = 1;
+    for (int n = 0; n < a.N; ++n) max_dim = std::max(max_dim, (int)a.dims[n]);
+    const FfSizes z = ffma_sizes(max_rank, max_dim, a.N);
+    const int64_t fixed = z.zbuf + z.wbuf + z.qf;
+    // as many warps per SM as fit with a ring of at least one largest step (at most 16); the ring takes the rest
+    int per_sm = 16;
+    while (per_sm > 1 && per_sm * (4 * (z.step + fixed) + kReservedPerCTA) > kSmemPerSM) --per_sm;
+    int64_t warp_floats = ((kSmemPerSM / per_sm - kReservedPerCTA) / 4) & ~int64_t(3);
+    warp_floats = std::min<int64_t>(warp_floats, kSmemPerCTA / 4);
+    FfArgs w;
+    w.zbuf = (int)z.zbuf;
+    w.wbuf = (int)z.wbuf;
+    w.ring = (int)((warp_floats - fixed) & ~int64_t(3));
+    w.warp_floats = (int)(w.ring + fixed);
+    w.slot = (int)(g_launches.fetch_add(1) % kSlots);
+    const size_t smem = sizeof(float) * (size_t)w.warp_floats;
+    cudaError_t e = cudaFuncSetAttribute(inner_ffma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(inner_ffma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess)
+        return e;
+    int dev = 0, sms = 0, occ = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, inner_ffma_kernel, 32, smem)) != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const int grid = std::min(a.B, sms * occ);
+    inner_ffma_kernel<<<grid, 32, smem, s>>>(a, w);
+    return cudaGetLastError();
+}
+
+}  // namespace ttc

@@ -200,7 +200,7 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     const bool uniform = hx.uniform && hy.uniform && hx.urank == hy.urank;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    // TTC_KERNEL=generic|fast|wpp forces the general-shape / CTA-per-pair / warp-per-pair kernel (cross-checks)
+    // TTC_KERNEL=generic|fast|wpp forces the general-shape / CTA-per-pair / warp-per-pair tensor-core kernel (cross-checks)
     const char* kv = std::getenv("TTC_KERNEL");
     const bool force_generic = kv && std::strcmp(kv, "generic") == 0;
     // uniform rank-16 trains with 16-byte aligned cores and trains: the specialised rank-16 kernel
@@ -217,7 +217,9 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
         e = ttc::launch_inner_r16(a, s);
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
         e = ttc::launch_inner_r64(a, s);
-    else if (!force_generic && !force_fast && (force_wpp || (hx.mult8 && hy.mult8)) && ttc::inner_wpp_supported(a, mr))
+    else if (!force_generic && !force_fast && !force_wpp && ttc::inner_ffma_supported(a, mr, hx.mult8 && hy.mult8))
+        e = ttc::launch_inner_ffma(a, mr, s);   // warp per pair on the FP32 pipe (ranks multiple of 8, <= 32)
+    else if (!force_generic && !force_fast && force_wpp && ttc::inner_wpp_supported(a, mr))
         e = ttc::launch_inner_wpp(a, mr, hx.mult8 && hy.mult8, s);   // warp per pair (ranks multiple of 8: full tiles)
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);

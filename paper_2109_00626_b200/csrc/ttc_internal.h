@@ -37,6 +37,8 @@ bool        inner_r64_supported(const InnerArgs& a, bool uniform_r64);
 bool        inner_wpp_supported(const InnerArgs& a, int max_rank);
 cudaError_t launch_inner_wpp(const InnerArgs& a, int max_rank, bool ranks_mult8, cudaStream_t s);
 cudaError_t launch_inner_r64(const InnerArgs& a, cudaStream_t s);
+bool        inner_ffma_supported(const InnerArgs& a, int max_rank, bool ranks_mult8);
+cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s);
 
 // ---- tt_contract (ladder) ------------------------------------------------------------------------
 enum ElKind : int32_t { EL_XFREE = 1, EL_YFREE = 2, EL_T = 3 };

@@ -237,3 +237,31 @@ def test_sharded_inner_nccl_single_rank():
         assert torch.equal(torch.cat(parts), full)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_ffma_rank_mult8_shapes(case):
+    """The FP32 warp-per-pair kernel (interior ranks multiples of 8, <= 32): random rank profiles over every
+    {8, 16, 24, 32} combination, mixed and odd mode sizes (boundary cores of odd size are copied without
+    cp.async), N = 2 (no interior step), N = 3, uniform ranks (ranks_host NULL), and ragged batch sizes."""
+    rng = np.random.default_rng(100 + case)
+    dims = [(2, 2, 2, 2, 2, 2), (3, 1, 5, 2, 7), (2, 2), (4, 3, 2), (2,) * 24, (1, 2, 3, 4, 5, 6, 7)][case]
+    B = [1, 5, 33, 130, 517, 64][case]
+    N = len(dims)
+    def ranks():
+        r = rng.choice([8, 16, 24, 32], size=(B, N + 1)).astype(np.int32)
+        r[:, 0] = 1
+        r[:, -1] = 1
+        return r
+    X = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, ranks(), dims, "geo")
+    Y = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 1, 0, ranks(), dims, "geo")
+    got = _run(X, Y)
+    _check(X, Y, got, _sample(B, 40, case), "edge")
+    got = _run(X, X)
+    _check(X, X, got, _sample(B, 40, case + 1), "self")
+    # uniform ranks through the ranks_host == NULL path
+    R = [8, 16, 24, 32, 24, 8][case]
+    ur = np.tile(np.array([1] + [R] * (N - 1) + [1], np.int32), (B, 1))
+    Xu = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, ur, dims, "geo")
+    got = _run(Xu, Xu)
+    _check(Xu, Xu, got, _sample(B, 24, case + 2), "self")
