@@ -146,14 +146,15 @@ __device__ __forceinline__ void block_fma(const float* __restrict__ A, int sA, c
     for (int a = 0; a < TA; ++a) za[a] = ld4(Ap[a]);
 #pragma unroll
     for (int b = 0; b < NB; ++b) fb[b] = ld4(Bp[b]);
+    // the iteration for the last chunk prefetches k = K: the 4 padding floats after every row / column (in
+    // bounds, discarded)
 #pragma unroll 2
     for (int k = 4; k <= K; k += 4) {
         float4 zn[TA], fn[NB];
-        const int kk = k < K ? k : 0;   // the last iteration re-reads chunk 0 (in bounds, discarded)
 #pragma unroll
-        for (int a = 0; a < TA; ++a) zn[a] = ld4(Ap[a] + kk);
+        for (int a = 0; a < TA; ++a) zn[a] = ld4(Ap[a] + k);
 #pragma unroll
-        for (int b = 0; b < NB; ++b) fn[b] = ld4(Bp[b] + kk);
+        for (int b = 0; b < NB; ++b) fn[b] = ld4(Bp[b] + k);
 #pragma unroll
         for (int a = 0; a < TA; ++a)
 #pragma unroll
@@ -172,21 +173,26 @@ __device__ __forceinline__ void block_fma(const float* __restrict__ A, int sA, c
     }
 }
 
-// out = A B^T over rows < 8 TA and columns < 4 ncols (ncols even), in blocks of 4 columns per lane.
+// All column blocks of one row count: 4 lane-columns per block, a 2-column tail.
+template <int TA>
+__device__ __forceinline__ void gemm_rows(const float* A, int sA, const float* B, int sB, int K, int ncols, float* out,
+                                          int rs, int cs, int ci, unsigned idiv, int lg, int lf) {
+    int cb = 0;
+    for (; cb + 4 <= ncols; cb += 4) block_fma<TA, 4>(A, sA, B, sB, K, out, rs, cs, ci, idiv, 4 * cb, lg, lf);
+    if (cb < ncols) block_fma<TA, 2>(A, sA, B, sB, K, out, rs, cs, ci, idiv, 4 * cb, lg, lf);
+}
+
+// out = A B^T over rows < 8 TA and columns < 4 ncols (ncols even); one dispatch on the row count per GEMM.
 __device__ __noinline__ void ff_gemm(const float* A, int sA, const float* B, int sB, int K, int TA, int ncols,
                                      float* out, int rs, int cs, int ci, unsigned idiv, int lane) {
     const int lg = lane >> 2, lf = lane & 3;
     A += lg * sA;
-    for (int cb = 0; cb < ncols; cb += 4) {
-        const int c0 = 4 * cb;
-#define FF_CASE(ta, nb) \
-    case 2 * (ta) + (nb) / 4 - 1: block_fma<ta, nb>(A, sA, B, sB, K, out, rs, cs, ci, idiv, c0, lg, lf); break;
-        switch (2 * TA + (ncols - cb >= 4 ? 1 : 0) - 1) {
-            FF_CASE(1, 2) FF_CASE(1, 4) FF_CASE(2, 2) FF_CASE(2, 4)
-            FF_CASE(3, 2) FF_CASE(3, 4) FF_CASE(4, 2) FF_CASE(4, 4)
-            default: break;
-        }
-#undef FF_CASE
+    if (TA >= 3) {
+        if (TA == 4) gemm_rows<4>(A, sA, B, sB, K, ncols, out, rs, cs, ci, idiv, lg, lf);
+        else gemm_rows<3>(A, sA, B, sB, K, ncols, out, rs, cs, ci, idiv, lg, lf);
+    } else {
+        if (TA == 2) gemm_rows<2>(A, sA, B, sB, K, ncols, out, rs, cs, ci, idiv, lg, lf);
+        else gemm_rows<1>(A, sA, B, sB, K, ncols, out, rs, cs, ci, idiv, lg, lf);
     }
 }
 
