@@ -165,6 +165,84 @@ __device__ __forceinline__ float cprime(const FreeCore& f, const float* TL, int 
     }
 }
 
+// 4 FMAs of one alpha-quad column against one scalar, packed (FFMA2: two FMAs per issue slot).
+__device__ __forceinline__ void quad_fma(float4& v, const float4 t, float g) {
+    unsigned long long lo, hi, tlo, thi, gg;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(lo) : "f"(v.x), "f"(v.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(hi) : "f"(v.z), "f"(v.w));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(tlo) : "f"(t.x), "f"(t.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(thi) : "f"(t.z), "f"(t.w));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(gg) : "f"(g));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(lo) : "l"(tlo), "l"(gg));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(hi) : "l"(thi), "l"(gg));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(lo));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.z), "=f"(v.w) : "l"(hi));
+}
+
+// Fast emission of one free core (no right absorption): every thread owns one alpha-quad of one mode index i
+// and walks the output columns beta = rr + Bs pp in steps of nb = blockDim / Q, writing one 16-byte streaming
+// store per column; consecutive threads write consecutive 16-byte chunks.  KIND: 0 X (x) I, 1 TL (X (x) I),
+// 2 I (x) Y, 3 TL (I (x) Y).  The free core's column it reads is contiguous along the summed bond.
+template <int KIND>
+__device__ __forceinline__ void emit_fast(const FreeCore& f, const float* TL, int Aout, int Bout, int Q, int Bs,
+                                          float* dst) {
+    const int I = f.I, R = f.Rb;
+    const int qpa = Aout >> 2, nb = blockDim.x / Q;
+    const int t = threadIdx.x;
+    if (t >= nb * Q) return;
+    const int a0 = 4 * (t % qpa), i = (t / qpa) % I;
+    int beta = t / Q;
+    int rr = beta % Bs, pp = beta / Bs;
+    const int blk = KIND < 2 ? R : f.H;
+    const int pblk = a0 / blk, roff = a0 - blk * pblk;   // this quad's rows: roff.. of block pblk
+    float* d = dst + a0 + (int64_t)Aout * (i + (int64_t)I * beta);
+    const int64_t dstep = (int64_t)Aout * I * nb;
+    const int rstep = nb % Bs, pstep = nb / Bs;
+    const float* gbase = f.G + R * i;                    // column (i, c) of the free core at gbase + R I c
+    const int gstride = R * I;
+    const int hs = Aout * f.H;
+    for (; beta < Bout; beta += nb, d += dstep) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (KIND == 0) {          // rows r + R pp carry X[r, i, rr]
+            if (pp == pblk) v = *reinterpret_cast<const float4*>(gbase + gstride * rr + roff);
+        } else if (KIND == 1) {   // sum_r TL[a0.., r + R pp] X[r, i, rr]
+            const float* gcol = gbase + gstride * rr;
+            const float* tl = TL + a0 + Aout * (R * pp);
+            float4 v2 = v;
+            for (int r = 0; r < R; r += 4) {
+                const float4 g = *reinterpret_cast<const float4*>(gcol + r);
+                quad_fma(v, *reinterpret_cast<const float4*>(tl + Aout * r), g.x);
+                quad_fma(v2, *reinterpret_cast<const float4*>(tl + Aout * (r + 1)), g.y);
+                quad_fma(v, *reinterpret_cast<const float4*>(tl + Aout * (r + 2)), g.z);
+                quad_fma(v2, *reinterpret_cast<const float4*>(tl + Aout * (r + 3)), g.w);
+            }
+            v.x += v2.x; v.y += v2.y; v.z += v2.z; v.w += v2.w;
+        } else if (KIND == 2) {   // rows rr + H p carry Y[p, j, pp]: this quad holds row rr + H pblk if any
+            const int k = rr - roff;
+            if ((unsigned)k < 4u) {
+                const float val = gbase[gstride * pp + pblk];
+                v.x = k == 0 ? val : 0.f; v.y = k == 1 ? val : 0.f; v.z = k == 2 ? val : 0.f; v.w = k == 3 ? val : 0.f;
+            }
+        } else {                  // sum_p TL[a0.., rr + H p] Y[p, j, pp]
+            const float* gcol = gbase + gstride * pp;
+            const float* tl = TL + a0 + Aout * rr;
+            float4 v2 = v;
+            for (int q = 0; q < R; q += 4) {
+                const float4 g = *reinterpret_cast<const float4*>(gcol + q);
+                quad_fma(v, *reinterpret_cast<const float4*>(tl + hs * q), g.x);
+                quad_fma(v2, *reinterpret_cast<const float4*>(tl + hs * (q + 1)), g.y);
+                quad_fma(v, *reinterpret_cast<const float4*>(tl + hs * (q + 2)), g.z);
+                quad_fma(v2, *reinterpret_cast<const float4*>(tl + hs * (q + 3)), g.w);
+            }
+            v.x += v2.x; v.y += v2.y; v.z += v2.z; v.w += v2.w;
+        }
+        st_cs4(d, v.x, v.y, v.z, v.w);
+        rr += rstep;
+        pp += pstep;
+        if (rr >= Bs) { rr -= Bs; ++pp; }
+    }
+}
+
 __device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* xc, const float* yc, int l,
                           const float* TL, const float* TR, float* out) {
     const OutCore& oc = a.outc[l];
@@ -185,123 +263,22 @@ __device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* 
     const int I = f.I;
     const int64_t total = (int64_t)Aout * I * Bout;
     float* dst = out + c.oo[l];
-    const bool quad_ok = (Aout % 4 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) && total < (1ll << 31);
-    if (!has_tr && quad_ok) {
-        // 4 consecutive alpha of one column per thread -> one 16-byte streaming store; consecutive threads write
-        // consecutive quads (coalesced).  Column / row decompositions by precomputed magic-number division.
-        const int qpc = Aout / 4;
-        const FastDiv dq = c.fd[0], di = c.fd[1], db = c.fd[2], dh = c.fd[3];
-        const uint32_t nq = (uint32_t)(total / 4);
-        const int Bsplit = f.xfree ? f.Rn : f.H;   // beta = rr + Bsplit * pp
-        // When blockDim is a multiple of qpc each thread keeps one alpha-quad a0 and walks the columns
-        // col = i + I * (rr + Bsplit * pp) in steps of blockDim / qpc: (i, rr, pp) are updated incrementally,
-        // no division inside the loop.  Otherwise every quad is decomposed by magic-number division.
-        const bool walk = (blockDim.x % qpc) == 0;
-        const uint32_t cstep = blockDim.x / qpc;                 // columns advanced per iteration (walk)
-        const int step_i = (int)(cstep % (uint32_t)I), step_b = (int)(cstep / (uint32_t)I);
-        const int step_rr = step_b % Bsplit, step_pp = step_b / Bsplit;
-        int a0 = 0, i = 0, rr = 0, pp = 0;
-        {
-            const uint32_t q0 = threadIdx.x;
-            const uint32_t col = dq.div(q0);
-            a0 = (int)(q0 - col * qpc) * 4;
-            const uint32_t beta = di.div(col);
-            i = (int)(col - beta * I);
-            const uint32_t pq = db.div(beta);
-            pp = (int)pq;
-            rr = (int)(beta - pq * Bsplit);
-        }
-        const int d_pb = (int)dh.div((uint32_t)a0);   // walk: this thread's alpha-quad block (fixed)
-        for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
-            if (!walk) {
-                const uint32_t col = dq.div(q);
-                a0 = (int)(q - col * qpc) * 4;
-                const uint32_t beta = di.div(col);
-                i = (int)(col - beta * I);
-                const uint32_t pq = db.div(beta);
-                pp = (int)pq;
-                rr = (int)(beta - pq * Bsplit);
-            }
-            float v[4];
-            if (f.xfree) {   // [r + R p, i, r' + R' p'] = X[r, i, r'] delta_{p p'}
-                const float* gcol = f.G + f.Rb * (i + I * rr);
-                if (has_tl) {   // two accumulators (even / odd r): half the dependent-FMA chain
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), ac2 = acc;
-                    const float* tl = TL + a0 + Aout * (f.Rb * pp);
-                    int r = 0;
-                    for (; r + 1 < f.Rb; r += 2) {
-                        const float g = gcol[r], g2 = gcol[r + 1];
-                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * r);
-                        const float4 t2 = *reinterpret_cast<const float4*>(tl + Aout * (r + 1));
-                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
-                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
-                        ac2.x = fmaf(t2.x, g2, ac2.x); ac2.y = fmaf(t2.y, g2, ac2.y);
-                        ac2.z = fmaf(t2.z, g2, ac2.z); ac2.w = fmaf(t2.w, g2, ac2.w);
-                    }
-                    if (r < f.Rb) {
-                        const float g = gcol[r];
-                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * r);
-                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
-                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
-                    }
-                    v[0] = acc.x + ac2.x; v[1] = acc.y + ac2.y; v[2] = acc.z + ac2.z; v[3] = acc.w + ac2.w;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int r = a0 + k - f.Rb * pp;
-                        v[k] = (r >= 0 && r < f.Rb) ? gcol[r] : 0.0f;
-                    }
-                }
-            } else {         // [r + H p, j, r' + H p'] = delta_{r r'} Y[p, j, p']
-                const float* gcol = f.G + f.Rb * (i + I * pp);
-                if (has_tl) {   // two accumulators (even / odd p)
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), ac2 = acc;
-                    const float* tl = TL + a0 + Aout * rr;
-                    int p = 0;
-                    for (; p + 1 < f.Rb; p += 2) {
-                        const float g = gcol[p], g2 = gcol[p + 1];
-                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * f.H * p);
-                        const float4 t2 = *reinterpret_cast<const float4*>(tl + Aout * f.H * (p + 1));
-                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
-                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
-                        ac2.x = fmaf(t2.x, g2, ac2.x); ac2.y = fmaf(t2.y, g2, ac2.y);
-                        ac2.z = fmaf(t2.z, g2, ac2.z); ac2.w = fmaf(t2.w, g2, ac2.w);
-                    }
-                    if (p < f.Rb) {
-                        const float g = gcol[p];
-                        const float4 t = *reinterpret_cast<const float4*>(tl + Aout * f.H * p);
-                        acc.x = fmaf(t.x, g, acc.x); acc.y = fmaf(t.y, g, acc.y);
-                        acc.z = fmaf(t.z, g, acc.z); acc.w = fmaf(t.w, g, acc.w);
-                    }
-                    v[0] = acc.x + ac2.x; v[1] = acc.y + ac2.y; v[2] = acc.z + ac2.z; v[3] = acc.w + ac2.w;
-                } else if (f.H >= 4) {
-                    // alpha = r + H p is nonzero only for r = r': within 4 consecutive alpha at most one hit
-                    const int pb = walk ? d_pb : (int)dh.div((uint32_t)a0);
-                    const int k = rr - (a0 - pb * f.H);   // position of alpha = r' + H pb inside the quad
-                    const float val = ((unsigned)k < 4u && pb < f.Rb) ? gcol[pb] : 0.0f;
-                    v[0] = k == 0 ? val : 0.0f;
-                    v[1] = k == 1 ? val : 0.0f;
-                    v[2] = k == 2 ? val : 0.0f;
-                    v[3] = k == 3 ? val : 0.0f;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int d = a0 + k - rr;
-                        const int p = d >= 0 ? (int)dh.div((uint32_t)d) : -1;
-                        v[k] = (d >= 0 && d == p * f.H && p < f.Rb) ? gcol[p] : 0.0f;
-                    }
-                }
-            }
-            st_cs4(dst + 4 * (int64_t)q, v[0], v[1], v[2], v[3]);
-            if (walk) {   // advance (i, rr, pp) by cstep columns
-                i += step_i;
-                int carry = 0;
-                if (i >= I) { i -= I; carry = 1; }
-                rr += step_rr + carry;
-                int carry2 = 0;
-                while (rr >= Bsplit) { rr -= Bsplit; ++carry2; }
-                pp += step_pp + carry2;
-            }
+    const int qpa = Aout >> 2;                              // alpha-quads per column
+    const int Q = qpa * I;                                  // threads per output column group (one beta)
+    const int Bs = f.xfree ? f.Rn : f.H;                    // beta = rr + Bs * pp
+    const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(f.G)) & 15u) == 0 &&
+                         ((reinterpret_cast<uintptr_t>(TL) & 15u) == 0);
+    // fast path: every thread owns one alpha-quad of one mode index i and walks beta in steps of nb; the free
+    // core's column (i, rr) / (i, pp) it reads is contiguous along the summed bond (16-byte loads)
+    const bool fast = !has_tr && (Aout & 3) == 0 && (f.Rb & 3) == 0 && aligned && Q <= (int)blockDim.x &&
+                      (f.xfree ? true : (f.H & 3) == 0) && total < (1ll << 31);
+    if (fast) {
+        const int kind = (f.xfree ? 0 : 2) + (has_tl ? 1 : 0);
+        switch (kind) {
+            case 0: emit_fast<0>(f, TL, Aout, Bout, Q, Bs, dst); break;
+            case 1: emit_fast<1>(f, TL, Aout, Bout, Q, Bs, dst); break;
+            case 2: emit_fast<2>(f, TL, Aout, Bout, Q, Bs, dst); break;
+            default: emit_fast<3>(f, TL, Aout, Bout, Q, Bs, dst); break;
         }
         return;
     }
