@@ -409,9 +409,11 @@ cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s) 
     const FfSizes z = ffma_sizes(max_rank, max_dim, a.N);
     const int64_t fixed = z.zbuf + z.wbuf + z.qf;
     // as many warps per SM as fit with a ring of at least one largest step (at most 16); the ring takes the rest
+    // (shared memory is allocated per CTA in 256-byte units, plus 1 KB reserved per CTA)
+    auto cta_bytes = [](int64_t floats) { return ((4 * floats + 255) & ~int64_t(255)) + kReservedPerCTA; };
     int per_sm = 16;
-    while (per_sm > 1 && per_sm * (4 * (z.step + fixed) + kReservedPerCTA) > kSmemPerSM) --per_sm;
-    int64_t warp_floats = ((kSmemPerSM / per_sm - kReservedPerCTA) / 4) & ~int64_t(3);
+    while (per_sm > 1 && per_sm * cta_bytes(z.step + fixed) > kSmemPerSM) --per_sm;
+    int64_t warp_floats = (((kSmemPerSM / per_sm - kReservedPerCTA) & ~int64_t(255)) / 4);
     warp_floats = std::min<int64_t>(warp_floats, kSmemPerCTA / 4);
     FfArgs w;
     w.zbuf = (int)z.zbuf;
