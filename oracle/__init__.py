@@ -52,6 +52,9 @@ def lib():
         L.oracle_tt_contract.argtypes = [c_int, _i32p, _i32p, _f64p, c_int, _i32p, _i32p, _f64p, c_int, _i32p, _i32p,
                                          ctypes.POINTER(ctypes.c_int32), _i32p, _i32p, _i32p, _i32p, c_i64pp,
                                          ctypes.c_void_p, c_i64pp, c_i64pp]
+        L.oracle_tt_splice.argtypes = [c_int, _i32p, _i32p, _f64p, c_int, _i32p, _i32p, _f64p, c_int, c_int,
+                                       ctypes.POINTER(ctypes.c_int32), _i32p, _i32p, _i32p, _i32p, c_i64pp,
+                                       ctypes.c_void_p]
         L.oracle_tt_inner_batch.argtypes = [c_int, c_int, _i32p, _i32p, _i64p, _f32p, _i32p, _i64p, _f32p, _f64p,
                                             c_int]
         L.oracle_tt_contract_batch.argtypes = [c_int, c_int, _i32p, _i32p, _i64p, _f32p, c_int, _i32p, _i32p, _i64p,
@@ -173,6 +176,35 @@ def tt_contract(xcores, ycores, x_modes, y_modes, with_cores: bool = True):
             cores.append(buf[pos:pos + a * i * b].reshape((a, i, b), order="F"))
             pos += a * i * b
         res.update(cores=cores, flat=buf, t_macs=tm.value, a_macs=am.value)
+    return res
+
+
+def tt_splice(xcores, ycores, n: int, m: int, with_cores: bool = True):
+    """O5: X x_n^m Y for end modes (n in {1, N}, m in {1, M}, 1-based) as the paper's TTCP splice (Alg. 2 steps
+    4-5).  Same result dict as tt_contract (order, dims, ranks, src, perm, elems, cores, flat)."""
+    xd, xr, xf = _train(xcores)
+    yd, yr, yf = _train(ycores)
+    Lmax = len(xd) + len(yd)
+    L = ctypes.c_int32(0)
+    od, ork, osrc, operm = (np.zeros(Lmax + 1, np.int32) for _ in range(4))
+    ne = ctypes.c_int64(0)
+    lb = lib()
+    _chk(lb.oracle_tt_splice(len(xd), xd, xr, xf, len(yd), yd, yr, yf, int(n), int(m), ctypes.byref(L), od, ork,
+                             osrc, operm, ctypes.byref(ne), None))
+    res = dict(order=L.value, dims=od[:L.value].copy(), ranks=ork[:L.value + 1].copy(), src=osrc[:L.value].copy(),
+               perm=operm[:L.value].copy(), elems=ne.value)
+    if with_cores:
+        buf = np.zeros(ne.value, dtype=np.float64)
+        _chk(lb.oracle_tt_splice(len(xd), xd, xr, xf, len(yd), yd, yr, yf, int(n), int(m), ctypes.byref(L), od, ork,
+                                 osrc, operm, ctypes.byref(ne), buf.ctypes.data))
+        cores, pos = [], 0
+        if L.value == 0:
+            cores = [buf[0]]
+        for l in range(L.value):
+            a, i, b = int(ork[l]), int(od[l]), int(ork[l + 1])
+            cores.append(buf[pos:pos + a * i * b].reshape((a, i, b), order="F"))
+            pos += a * i * b
+        res.update(cores=cores, flat=buf)
     return res
 
 

@@ -26,6 +26,11 @@
  *                                "ladder" of SURVEY.md Appendix A; readings R7-R10).  Free cores
  *                                are materialised as dense Kronecker products with identities, transfers
  *                                T_k as dense matrices, and absorbed by plain matrix products.
+ *   oracle_tt_splice        O5   single-mode contraction of END modes (n in {1, N}, m in {1, M}) as the paper's
+ *                                own TTCP splice (Alg. 2 steps 4-5, Example 1 PAPER.md:313-322):
+ *                                K = A_x^T A_y (Eq. 12), then the X cores (reversed with rank modes swapped when
+ *                                n = 1), K, then the Y cores (reversed when m = M); K absorbed into the next core
+ *                                (readings R6, R10).  Ranks stay R and P (no Kronecker bonds).
  *   oracle_tt_inner_batch / oracle_tt_contract_batch: loops of the above over a batch of pairs
  *                                (OpenMP over pairs) -- the CPU baseline bench.py times.
  */
@@ -424,6 +429,111 @@ int oracle_tt_contract(int N, const int32_t* xdims, const int32_t* xr, const dou
         memcpy(outp, prev_core, sizeof(double) * prev_a * prev_i * prev_b);
         free(prev_core);
     }
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------- O5: TTCP splice of end modes */
+/* Z = X x_n^m Y for n in {1, N}, m in {1, M} (1-based), as a TT in the order of Alg. 2 step 5
+ * (PAPER.md:363-374): the X free cores -- reversed, N..2, each core transposed in its rank modes, when n = 1
+ * (the B_x x_2^1 G_x^(N-1) ... G_x^(2) chain of step 5); in order 1..N-1 when n = N -- then
+ * K = A_x^T A_y (step 4, Eq. 12), then the Y free cores (2..M when m = 1; reversed M-1..1, transposed, when
+ * m = M).  A_x is the contracted X core read as I x R (its one non-unit bond), A_y likewise.  K is absorbed
+ * into the next core of the chain by a plain matrix product (reading R10), else into the previous one; with no
+ * free core at all the result is the scalar K.  Same outputs as oracle_tt_contract (src, perm: canonical Eq. 8
+ * order, X free ascending then Y free ascending). */
+int oracle_tt_splice(int N, const int32_t* xdims, const int32_t* xr, const double* xc,
+                     int M, const int32_t* ydims, const int32_t* yr, const double* yc, int n, int m,
+                     int32_t* out_order, int32_t* out_dims, int32_t* out_ranks, int32_t* out_src,
+                     int32_t* out_perm, int64_t* out_elems, double* out_cores)
+{
+    if (N < 1 || M < 1 || N > 256 || M > 256) return OR_ERR_ARG;
+    if (xr[0] != 1 || xr[N] != 1 || yr[0] != 1 || yr[M] != 1) return OR_ERR_ARG;
+    if ((n != 1 && n != N) || (m != 1 && m != M)) return OR_ERR_MODES;
+    if (xdims[n - 1] != ydims[m - 1]) return OR_ERR_SHAPE;
+    int64_t xoff[257], yoff[257];
+    xoff[0] = 0; for (int k = 0; k < N; ++k) xoff[k + 1] = xoff[k] + (int64_t)xr[k] * xdims[k] * xr[k + 1];
+    yoff[0] = 0; for (int k = 0; k < M; ++k) yoff[k + 1] = yoff[k] + (int64_t)yr[k] * ydims[k] * yr[k + 1];
+    /* the chain of free cores: source (+x / -y, 0-based mode), reversed? */
+    int src[512], rev[512], L = 0;
+    if (n == 1) for (int k = N - 1; k >= 1; --k) { src[L] = k + 1; rev[L] = 1; ++L; }
+    else        for (int k = 0; k < N - 1; ++k) { src[L] = k + 1; rev[L] = 0; ++L; }
+    const int nx = L;   /* K sits between chain positions nx - 1 and nx */
+    if (m == 1) for (int k = 1; k < M; ++k) { src[L] = -(k + 1); rev[L] = 0; ++L; }
+    else        for (int k = M - 2; k >= 0; --k) { src[L] = -(k + 1); rev[L] = 1; ++L; }
+    /* K = A_x^T A_y: A_x[i, r] is X_1[0, i, r] (n = 1) or X_N[r, i, 0] (n = N) */
+    const int I = xdims[n - 1];
+    const int Rk = (n == 1) ? xr[1] : xr[N - 1], Pk = (m == 1) ? yr[1] : yr[M - 1];
+    const double* Ax = xc + xoff[n - 1];
+    const double* Ay = yc + yoff[m - 1];
+    double* Km = (double*)malloc(sizeof(double) * Rk * Pk);   /* Km[r + Rk p] */
+    for (int p = 0; p < Pk; ++p)
+        for (int r = 0; r < Rk; ++r) {
+            double acc = 0.0;
+            for (int i = 0; i < I; ++i) {
+                const double a = (n == 1) ? Ax[i + I * r] : Ax[r + Rk * i];
+                const double b = (m == 1) ? Ay[i + I * p] : Ay[p + Pk * i];
+                acc += a * b;
+            }
+            Km[r + Rk * p] = acc;
+        }
+    /* metadata */
+    *out_order = L;
+    out_ranks[0] = 1;
+    for (int l = 0; l < L; ++l) {
+        const int s = src[l] > 0 ? src[l] - 1 : -src[l] - 1;
+        const int32_t* rr = src[l] > 0 ? xr : yr;
+        out_dims[l] = src[l] > 0 ? xdims[s] : ydims[s];
+        out_src[l] = src[l];
+        out_ranks[l + 1] = rev[l] ? rr[s] : rr[s + 1];
+    }
+    if (L > 0) {
+        /* the bond at K: the left core's right rank is Rk, the right core's left rank Pk; K's rows (cols) replace
+           it on the side it is absorbed into */
+        if (nx < L) out_ranks[nx] = (nx == 0) ? 1 : Rk;   /* absorbed into chain core nx: its left bond becomes Rk */
+        out_ranks[L] = 1;
+    }
+    {
+        int c = 0;
+        for (int k = 1; k <= N; ++k) for (int q = 0; q < L; ++q) if (out_src[q] == k) out_perm[c++] = q + 1;
+        for (int k = 1; k <= M; ++k) for (int q = 0; q < L; ++q) if (out_src[q] == -k) out_perm[c++] = q + 1;
+    }
+    int64_t total = 0;
+    for (int l = 0; l < L; ++l) total += (int64_t)out_ranks[l] * out_dims[l] * out_ranks[l + 1];
+    *out_elems = (L == 0) ? 1 : total;
+    if (!out_cores) { free(Km); return OR_OK; }
+    if (L == 0) { out_cores[0] = Km[0]; free(Km); return OR_OK; }
+    /* numeric: each chain core as a dense (A x I x B) array, K absorbed by a plain matrix product */
+    double* outp = out_cores;
+    for (int l = 0; l < L; ++l) {
+        const int s = src[l] > 0 ? src[l] - 1 : -src[l] - 1;
+        const int32_t* rr = src[l] > 0 ? xr : yr;
+        const double* G = (src[l] > 0 ? xc + xoff[s] : yc + yoff[s]);
+        const int64_t a0 = rr[s], Id = src[l] > 0 ? xdims[s] : ydims[s], b0 = rr[s + 1];
+        const int64_t A = rev[l] ? b0 : a0, B = rev[l] ? a0 : b0;
+        double* C = (double*)malloc(sizeof(double) * A * Id * B);   /* C[u, i, v] at u + A (i + Id v) */
+        for (int64_t v = 0; v < B; ++v)
+            for (int64_t i = 0; i < Id; ++i)
+                for (int64_t u = 0; u < A; ++u)
+                    C[u + A * (i + Id * v)] = rev[l] ? G[v + a0 * (i + Id * u)] : G[u + a0 * (i + Id * v)];
+        if (l == nx) {               /* left absorption: C'[r, i, v] = sum_p K[r, p] C[p, i, v] */
+            double* Cn = (double*)malloc(sizeof(double) * Rk * Id * B);
+            matmul(Rk, A, Id * B, Km, C, Cn, NULL);
+            free(C); C = Cn;
+            memcpy(outp, C, sizeof(double) * Rk * Id * B);
+            outp += Rk * Id * B;
+        } else if (l == L - 1 && nx == L) {   /* no core after K: right absorption C'[u, i, p] = sum_r C[u, i, r] K[r, p] */
+            double* Cn = (double*)malloc(sizeof(double) * A * Id * Pk);
+            matmul(A * Id, B, Pk, C, Km, Cn, NULL);
+            memcpy(outp, Cn, sizeof(double) * A * Id * Pk);
+            outp += A * Id * Pk;
+            free(Cn);
+        } else {
+            memcpy(outp, C, sizeof(double) * A * Id * B);
+            outp += A * Id * B;
+        }
+        free(C);
+    }
+    free(Km);
     return OR_OK;
 }
 
