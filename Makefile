@@ -17,7 +17,7 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 
 build/%.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p build
-	$(NVCC) -O2 -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -x cu $(ARCH) -c $< -o $@
+	$(NVCC) -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Xcompiler -O3 -x cu $(ARCH) -c $< -o $@
 
 $(PKG)/libttc.so: $(OBJS)
 	$(NVCC) -shared $(ARCH) -o $@ $(OBJS) -cudart static

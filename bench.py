@@ -48,6 +48,34 @@ def parse():
     return p.parse_args()
 
 
+# floats of one pair's output train (uniform-rank contraction workloads): C3 ladder,
+# S1 splice (chain X6^T .. X2^T, K Y2, Y3 .. Y6 of rank 8, I = 8)
+PAIR_OUT = {"C3": 102976, "S1": 4224}
+
+
+def _oracle_pairs(cfg, X, Y, count, nthreads):
+    """The oracle (as it stands) on the first `count` pairs of (X, Y) for workload cfg."""
+    import oracle
+    c = ttgen.CONFIGS[cfg]
+    if cfg in PAIR_OUT:
+        per = PAIR_OUT[cfg]
+        offs = np.arange(count, dtype=np.int64) * per
+        if c["op"] == "splice":
+            oracle.tt_splice_batch(X, Y, c["x_mode"], c["y_mode"], offs, per * count, nthreads, 0, count)
+        else:
+            oracle.tt_contract_batch(X, Y, list(c["x_modes"]), list(c["y_modes"]), offs, per * count, nthreads, 0,
+                                     count)
+    else:
+        xc = np.ascontiguousarray(X.cores.detach().cpu().numpy(), dtype=np.float32)
+        yc = np.ascontiguousarray(Y.cores.detach().cpu().numpy(), dtype=np.float32)
+        oracle.tt_inner_batch_np(xc, yc, X, Y, nthreads, 0, count)
+
+
+def _oracle_name(cfg):
+    op = ttgen.CONFIGS[cfg]["op"]
+    return {"contract": "O3", "splice": "O5"}.get(op, "O2")
+
+
 def per_rank_pairs(cfg: str) -> int:
     c = ttgen.CONFIGS[cfg]
     # C4 / C5 are quoted "sharded over ... 8 GPUs": one GPU's share of the 8-way split is the per-GPU batch
@@ -114,23 +142,13 @@ def flop_peak_tflops(sm_max_mhz: float) -> float:
 
 
 # ------------------------------------------------------------------------------------------------ CPU legs
-def cpu_oracle_rate(cfg: str, X, Y, target_s: float, plan_meta=None):
+def cpu_oracle_rate(cfg: str, X, Y, target_s: float):
     """Time the oracle (as it stands) on a bounded prefix of this rank's pairs, all host cores."""
-    import oracle
     nthreads = len(os.sched_getaffinity(0))
-    xc = np.ascontiguousarray(X.cores.detach().cpu().numpy(), dtype=np.float32)
-    yc = np.ascontiguousarray(Y.cores.detach().cpu().numpy(), dtype=np.float32)
 
     def run(count):
         t0 = time.perf_counter()
-        if cfg == "C3":
-            c = ttgen.CONFIGS["C3"]
-            per = plan_meta
-            offs = np.arange(count, dtype=np.int64) * per
-            oracle.tt_contract_batch(X, Y, list(c["x_modes"]), list(c["y_modes"]), offs, per * count, nthreads, 0,
-                                     count)
-        else:
-            oracle.tt_inner_batch_np(xc, yc, X, Y, nthreads, 0, count)
+        _oracle_pairs(cfg, X, Y, count, nthreads)
         return time.perf_counter() - t0
 
     probe = max(1, min(X.B, nthreads))
@@ -143,7 +161,7 @@ def cpu_oracle_rate(cfg: str, X, Y, target_s: float, plan_meta=None):
         reps += 1
     return {"value": reps * count / t, "unit": UNIT, "cores": nthreads, "kind": "oracle",
             "sample": f"{reps} pass(es) over the first {count} of the rank's {X.B} {cfg} pairs (fp64 oracle "
-                      f"O{'3' if cfg == 'C3' else '2'}, OpenMP over pairs), {t:.1f} s"}, count, t / reps
+                      f"{_oracle_name(cfg)}, OpenMP over pairs), {t:.1f} s"}, count, t / reps
 
 
 def run_reference(args, rank, world):
@@ -153,24 +171,12 @@ def run_reference(args, rank, world):
     cfg = args.config
     B = args.pairs or per_rank_pairs(cfg)
     X, Y = ttgen.config_batch(cfg, "iid", 0, B, args.seed, "cpu")
-    meta = None
-    if cfg == "C3":
-        meta = 102976
     steps_budget = 150.0 / max(1, args.steps + args.warmup)
-    cb, count, t = cpu_oracle_rate(cfg, X, Y, min(args.cpu_seconds, steps_budget), meta)
+    cb, count, t = cpu_oracle_rate(cfg, X, Y, min(args.cpu_seconds, steps_budget))
     times = []
-    import oracle  # noqa: F401
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        if cfg == "C3":
-            c = ttgen.CONFIGS["C3"]
-            offs = np.arange(count, dtype=np.int64) * meta
-            oracle.tt_contract_batch(X, Y, list(c["x_modes"]), list(c["y_modes"]), offs, meta * count,
-                                     cb["cores"], 0, count)
-        else:
-            xc = np.ascontiguousarray(X.cores.numpy(), dtype=np.float32)
-            yc = np.ascontiguousarray(Y.cores.numpy(), dtype=np.float32)
-            oracle.tt_inner_batch_np(xc, yc, X, Y, cb["cores"], 0, count)
+        _oracle_pairs(cfg, X, Y, count, cb["cores"])
         if s >= args.warmup:
             times.append(time.perf_counter() - t0)
     ms = 1e3 * sum(times) / len(times)
@@ -227,6 +233,16 @@ def main():
         def step():
             ttc.ttc_contract(plan, XD, YD, out=out, stream=stream)
         kernel_name = "contract_kernel"
+    elif c["op"] == "splice":
+        plan = ttc.ttc_splice_plan_create(XD, YD, c["x_mode"], c["y_mode"])
+        out = torch.empty(plan.total, dtype=torch.float32, device=dev)
+        alg_bytes = 4.0 * (X.cores.numel() + Y.cores.numel()) + 4.0 * plan.total
+        # K = A_x^T A_y (I R_1 P_1 MACs) and its absorption into Y_2 (R_1 P_1 J_2 P_2 MACs), per pair
+        alg_flops = 2.0 * B * (c["I"] * c["R"] * c["P"] + c["R"] * c["P"] * c["I"] * c["P"])
+
+        def step():
+            ttc.ttc_contract(plan, XD, YD, out=out, stream=stream)
+        kernel_name = "splice_kernel"
     else:
         out = torch.empty(B, dtype=torch.float32, device=dev)
         mac, byts = ttc.ttc_pair_cost(XD, YD)
@@ -333,7 +349,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         Xh = ttgen.TTBatch(X.cores.cpu(), X.ranks, X.offsets, X.dims)
         Yh = ttgen.TTBatch(Y.cores.cpu(), Y.ranks, Y.offsets, Y.dims)
-        cb, _, _ = cpu_oracle_rate(cfg, Xh, Yh, args.cpu_seconds, 102976 if cfg == "C3" else None)
+        cb, _, _ = cpu_oracle_rate(cfg, Xh, Yh, args.cpu_seconds)
 
     if rank == 0:
         conf = {"workload": cfg, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in c.items() if k != "op"},

@@ -108,6 +108,23 @@ typedef struct ttc_contract_plan ttc_contract_plan;   /* opaque, host-only, immu
 ttc_status ttc_contract_plan_create(const ttc_tt_batch* x, const ttc_tt_batch* y, int32_t npairs,
                                     const int32_t* x_modes, const int32_t* y_modes, ttc_contract_plan** plan);
 
+/* ---------------------------------------------------------------------------------------------------
+ * ttc_splice_plan_create: the paper's own TTCP construction for one pair of END modes (Alg. 2 steps 4-5,
+ * PAPER.md:358-374; Example 1), for operands already in TT format: with x_mode in {1, N} and
+ * y_mode in {1, M} (1-based, I_{x_mode} = J_{y_mode}) the result Z = X x_n^m Y is the chain
+ *     [X free cores]  K = A_x^T A_y (Eq. 12)  [Y free cores]
+ * where the X free cores run N..2 with their rank modes swapped (core [s, i, r] = X_n[r, i, s]) when x_mode = 1
+ * and 1..N-1 unchanged when x_mode = N; the Y free cores run 2..M when y_mode = 1 and M-1..1 swapped when
+ * y_mode = M; A_x is the contracted X core read as I x R (its non-unit bond), A_y likewise.  K is absorbed into
+ * the first Y free core (from the left), else into the last X free core (from the right); N = M = 1 gives the
+ * scalar.  Output bonds are the operands' own ranks (no R*P Kronecker bonds as in the ladder), L = N + M - 2.
+ * The returned plan is used exactly like a contraction plan (query, layout, ttc_contract, destroy): out_src /
+ * out_perm give the chain order and the permutation to Eq. 8's order (Alg. 2 step 6).  Errors as
+ * ttc_contract_plan_create; an interior mode gives TTC_ERR_MODES (use ttc_contract_plan_create).
+ * ------------------------------------------------------------------------------------------------- */
+ttc_status ttc_splice_plan_create(const ttc_tt_batch* x, const ttc_tt_batch* y, int32_t x_mode, int32_t y_mode,
+                                  ttc_contract_plan** plan);
+
 /* Structural metadata (identical for every pair of the batch).  Any output pointer may be NULL.
  *   out_order : L;  out_dims[L] : mode sizes in ladder order;
  *   out_src[L] : +n (X mode n) or -m (Y mode m), 1-based;

@@ -59,6 +59,8 @@ def lib():
                                             c_int]
         L.oracle_tt_contract_batch.argtypes = [c_int, c_int, _i32p, _i32p, _i64p, _f32p, c_int, _i32p, _i32p, _i64p,
                                                _f32p, c_int, _i32p, _i32p, _i64p, _f64p, c_int]
+        L.oracle_tt_splice_batch.argtypes = [c_int, c_int, _i32p, _i32p, _i64p, _f32p, c_int, _i32p, _i32p, _i64p,
+                                             _f32p, c_int, c_int, _i64p, _f64p, c_int]
         L.oracle_max_threads.restype = c_int
         _lib = L
     return _lib
@@ -249,6 +251,22 @@ def tt_contract_batch(X, Y, x_modes, y_modes, out_offsets, total, nthreads: int 
         Y.N, _i32(Y.dims), np.ascontiguousarray(Y.ranks[first:first + count], np.int32),
         np.ascontiguousarray(Y.offsets[first:first + count], np.int64), yc,
         len(x_modes), _i32(x_modes), _i32(y_modes), np.ascontiguousarray(out_offsets, np.int64), out, nthreads))
+    return out
+
+
+def tt_splice_batch(X, Y, n: int, m: int, out_offsets, total, nthreads: int = 0, first: int = 0,
+                    count: int = None) -> np.ndarray:
+    """O5 over a batch; out_offsets[b] (relative to the returned buffer) from the caller's layout."""
+    count = X.B - first if count is None else count
+    xc = np.ascontiguousarray(X.cores.detach().cpu().numpy(), dtype=np.float32)
+    yc = np.ascontiguousarray(Y.cores.detach().cpu().numpy(), dtype=np.float32)
+    out = np.zeros(int(total), dtype=np.float64)
+    _chk(lib().oracle_tt_splice_batch(
+        count, X.N, _i32(X.dims), np.ascontiguousarray(X.ranks[first:first + count], np.int32),
+        np.ascontiguousarray(X.offsets[first:first + count], np.int64), xc,
+        Y.N, _i32(Y.dims), np.ascontiguousarray(Y.ranks[first:first + count], np.int32),
+        np.ascontiguousarray(Y.offsets[first:first + count], np.int64), yc,
+        int(n), int(m), np.ascontiguousarray(out_offsets, np.int64), out, nthreads))
     return out
 
 

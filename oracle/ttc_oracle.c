@@ -598,6 +598,33 @@ int oracle_tt_contract_batch(int B, int N, const int32_t* xdims, const int32_t* 
     return bad ? OR_ERR_ARG : OR_OK;
 }
 
+int oracle_tt_splice_batch(int B, int N, const int32_t* xdims, const int32_t* xranks, const int64_t* xoff,
+                           const float* xcores, int M, const int32_t* ydims, const int32_t* yranks,
+                           const int64_t* yoff, const float* ycores, int n, int m,
+                           const int64_t* out_off, double* out_cores, int nthreads)
+{
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic) reduction(| : bad)
+#endif
+    for (int b = 0; b < B; ++b) {
+        const int32_t* xr = xranks + (int64_t)b * (N + 1);
+        const int32_t* yr = yranks + (int64_t)b * (M + 1);
+        int64_t nx = 0, ny = 0;
+        for (int k = 0; k < N; ++k) nx += (int64_t)xr[k] * xdims[k] * xr[k + 1];
+        for (int k = 0; k < M; ++k) ny += (int64_t)yr[k] * ydims[k] * yr[k + 1];
+        double* X = widen(xcores + xoff[b], nx);
+        double* Y = widen(ycores + yoff[b], ny);
+        int32_t L, od[512], ork[513], os[512], op[512];
+        int64_t ne;
+        if (oracle_tt_splice(N, xdims, xr, X, M, ydims, yr, Y, n, m, &L, od, ork, os, op, &ne,
+                             out_cores + out_off[b]) != OR_OK) bad |= 1;
+        free(X); free(Y);
+    }
+    return bad ? OR_ERR_ARG : OR_OK;
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

@@ -33,7 +33,8 @@ TTC_OK, TTC_ERR_NULL, TTC_ERR_SHAPE, TTC_ERR_RANK, TTC_ERR_MODES = 0, 1, 2, 3, 4
 TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG = 5, 6, 7, 8, 9
 TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
 
-EXPORTED = ("ttc_inner", "ttc_contract_plan_create", "ttc_contract_plan_query", "ttc_contract_plan_layout",
+EXPORTED = ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
+            "ttc_contract_plan_layout",
             "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
             "ttc_last_error", "ttc_version")
 
@@ -49,6 +50,8 @@ _P = ctypes.POINTER
 _lib.ttc_inner.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p]
 _lib.ttc_contract_plan_create.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_int32, ctypes.c_void_p,
                                           ctypes.c_void_p, _P(ctypes.c_void_p)]
+_lib.ttc_splice_plan_create.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_void_p]
 _lib.ttc_contract_plan_query.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 6
 _lib.ttc_contract_plan_layout.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 _lib.ttc_contract.argtypes = [ctypes.c_void_p, _P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p,
@@ -61,7 +64,8 @@ _lib.ttc_status_string.restype = ctypes.c_char_p
 _lib.ttc_status_string.argtypes = [ctypes.c_int]
 _lib.ttc_last_error.restype = ctypes.c_char_p
 _lib.ttc_version.restype = ctypes.c_int32
-for _f in ("ttc_inner", "ttc_contract_plan_create", "ttc_contract_plan_query", "ttc_contract_plan_layout",
+for _f in ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
+           "ttc_contract_plan_layout",
            "ttc_contract", "ttc_pair_cost", "ttc_partition"):
     getattr(_lib, _f).restype = ctypes.c_int
 
@@ -220,6 +224,7 @@ class ContractPlan:
         _check(_lib.ttc_contract_plan_layout(handle, _ptr(self.ranks) if x.B else None,
                                              _ptr(self.offsets) if x.B else None))
         self._offsets_dev = None
+        self._uniform_out = None
 
     def __del__(self):
         if getattr(self, "handle", None):
@@ -233,6 +238,14 @@ def ttc_contract_plan_create(x: TTDevice, y: TTDevice, x_modes: Sequence[int], y
     h = ctypes.c_void_p(0)
     _check(_lib.ttc_contract_plan_create(ctypes.byref(x.c), ctypes.byref(y.c), len(xm), _ptr(xm) if len(xm) else None,
                                          _ptr(ym) if len(ym) else None, ctypes.byref(h)))
+    return ContractPlan(h.value, x, y)
+
+
+def ttc_splice_plan_create(x: TTDevice, y: TTDevice, x_mode: int, y_mode: int) -> ContractPlan:
+    """The paper's TTCP splice of one pair of end modes (ttc.h: ttc_splice_plan_create); use the plan like a
+    contraction plan (query / layout / ttc_contract)."""
+    h = ctypes.c_void_p(0)
+    _check(_lib.ttc_splice_plan_create(ctypes.byref(x.c), ctypes.byref(y.c), int(x_mode), int(y_mode), ctypes.byref(h)))
     return ContractPlan(h.value, x, y)
 
 
@@ -252,7 +265,9 @@ def ttc_contract(plan: ContractPlan, x: TTDevice, y: TTDevice, out: torch.Tensor
     """Output cores of every pair (ttc.h: ttc_contract) -> (cores float32 [total], ranks [B, L+1], offsets [B])."""
     if out is None:
         out = torch.empty(max(plan.total, 0), dtype=torch.float32, device=x.cores.device)
-    uniform_out = plan.B <= 1 or bool(np.all(plan.ranks == plan.ranks[0:1]))
+    if plan._uniform_out is None:
+        plan._uniform_out = plan.B <= 1 or bool(np.all(plan.ranks == plan.ranks[0:1]))
+    uniform_out = plan._uniform_out
     offs_dev = None
     if not uniform_out:
         if plan._offsets_dev is None or plan._offsets_dev.device != out.device:

@@ -38,6 +38,7 @@ struct HostTrain {
     int max_rank = 1;
     bool mult8 = true;                 // every interior rank is a multiple of 8
     int64_t train_elems_uniform = 0;   // uniform ranks: elements per train
+    std::vector<int64_t> sizes;        // heterogeneous ranks: elements of train b (valid ranks only)
 
     int rank(int b, int n) const {
         if (!uniform) return t->ranks_host[(int64_t)b * (N + 1) + n];
@@ -72,21 +73,42 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
         h->max_rank = t->order > 1 ? h->urank : 1;
     } else {
         if (t->batch > 0 && !t->ranks_dev) return fail(TTC_ERR_NULL, "%s: ranks_host given but ranks_dev is NULL", name);
-        int mr = 1;
+        // one branch-light pass over the interior ranks (this runs on every call: O(B N), e.g. 1M ranks for
+        // C5); the slow loop below only runs to name the first offending rank
+        int mr = 1, bad = 0;
+        unsigned or8 = 0;
+        const int N = t->order;
+        const int32_t* rh = t->ranks_host;
+        // the train sizes come out of the same pass (h->sizes): sizes and bounds are checked below
+        h->sizes.resize(t->batch);
         for (int b = 0; b < t->batch; ++b) {
-            const int32_t* r = t->ranks_host + (int64_t)b * (t->order + 1);
-            if (r[0] != 1 || r[t->order] != 1)
-                return fail(TTC_ERR_RANK, "%s pair %d: boundary ranks R_0 = %d, R_N = %d (must be 1)", name, b, r[0],
-                            r[t->order]);
-            for (int n = 1; n < t->order; ++n) {
-                if (r[n] < 1) return fail(TTC_ERR_RANK, "%s pair %d: rank R_%d = %d < 1", name, b, n, r[n]);
-                if (r[n] > TTC_MAX_RANK)
-                    return fail(TTC_ERR_UNSUPPORTED, "%s pair %d: rank R_%d = %d > %d", name, b, n, r[n], TTC_MAX_RANK);
-                mr = std::max(mr, (int)r[n]);
-                if (r[n] & 7) h->mult8 = false;
+            const int32_t* r = rh + (int64_t)b * (N + 1);
+            bad |= (r[0] != 1) | (r[N] != 1);
+            int64_t elems = (int64_t)t->dims[0] * r[1];
+            for (int n = 1; n < N; ++n) {
+                const int v = r[n];
+                bad |= (v < 1) | (v > TTC_MAX_RANK);
+                mr = v > mr ? v : mr;
+                or8 |= (unsigned)v;
+                elems += (int64_t)v * t->dims[n] * r[n + 1];
+            }
+            h->sizes[b] = elems;
+        }
+        if (bad) {
+            for (int b = 0; b < t->batch; ++b) {
+                const int32_t* r = rh + (int64_t)b * (N + 1);
+                if (r[0] != 1 || r[N] != 1)
+                    return fail(TTC_ERR_RANK, "%s pair %d: boundary ranks R_0 = %d, R_N = %d (must be 1)", name, b,
+                                r[0], r[N]);
+                for (int n = 1; n < N; ++n) {
+                    if (r[n] < 1) return fail(TTC_ERR_RANK, "%s pair %d: rank R_%d = %d < 1", name, b, n, r[n]);
+                    if (r[n] > TTC_MAX_RANK)
+                        return fail(TTC_ERR_UNSUPPORTED, "%s pair %d: rank R_%d = %d > %d", name, b, n, r[n], TTC_MAX_RANK);
+                }
             }
         }
-        h->max_rank = mr;
+        h->mult8 = (or8 & 7u) == 0;   // every interior rank is a multiple of 8
+        h->max_rank = N > 1 ? mr : 1;
     }
     if (t->offsets_host && t->batch > 0 && !t->offsets_dev)
         return fail(TTC_ERR_NULL, "%s: offsets_host given but offsets_dev is NULL", name);
@@ -96,20 +118,25 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
     if (t->batch > 0 && !t->cores) return fail(TTC_ERR_NULL, "%s: cores is NULL", name);
     if (t->cores && (reinterpret_cast<uintptr_t>(t->cores) & 3u))
         return fail(TTC_ERR_ALIGN, "%s: cores pointer not 4-byte aligned", name);
-    // sizes and bounds, overflow-checked
-    int64_t packed_end = 0;
-    for (int b = 0; b < t->batch; ++b) {
+    // sizes and bounds, overflow-checked.  A train has at most TTC_MAX_ORDER cores of at most
+    // TTC_MAX_RANK^2 * (2^31 - 1) elements, < 2^53: its size cannot overflow; offset + size can.
+    const int N = t->order;
+    if (h->uniform) {
         int64_t elems = 0;
-        if (b == 0 || !h->uniform) {
-            for (int n = 0; n < t->order; ++n) {
-                int64_t sz;
-                if (!mul_ok((int64_t)h->rank(b, n) * t->dims[n], h->rank(b, n + 1), &sz) || !add_ok(elems, sz, &elems))
-                    return fail(TTC_ERR_OVERFLOW, "%s pair %d: train size overflows int64", name, b);
-            }
-            if (h->uniform) h->train_elems_uniform = elems;
-        } else {
-            elems = h->train_elems_uniform;
-        }
+        for (int n = 0; n < N; ++n) elems += (int64_t)h->rank(0, n) * t->dims[n] * h->rank(0, n + 1);
+        h->train_elems_uniform = elems;
+    }
+    int64_t packed_end = 0;
+    if (!t->offsets_host && h->uniform && t->batch > 0) {   // packed uniform: the last train bounds everything
+        int64_t last;
+        if (!mul_ok(h->train_elems_uniform, t->batch, &last)) return fail(TTC_ERR_OVERFLOW, "%s: batch size overflows", name);
+        if (t->n_elems > 0 && last > t->n_elems)
+            return fail(TTC_ERR_OVERFLOW, "%s: %d packed trains of %lld floats exceed n_elems = %lld", name,
+                        t->batch, (long long)h->train_elems_uniform, (long long)t->n_elems);
+        return TTC_OK;
+    }
+    for (int b = 0; b < t->batch; ++b) {
+        const int64_t elems = h->uniform ? h->train_elems_uniform : h->sizes[b];
         int64_t start = t->offsets_host ? t->offsets_host[b] : packed_end, end;
         if (start < 0) return fail(TTC_ERR_OVERFLOW, "%s pair %d: offset %lld < 0", name, b, (long long)start);
         if (!add_ok(start, elems, &end)) return fail(TTC_ERR_OVERFLOW, "%s pair %d: offset + size overflows", name, b);
@@ -117,15 +144,6 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
             return fail(TTC_ERR_OVERFLOW, "%s pair %d: train [%lld, %lld) runs past n_elems = %lld", name, b,
                         (long long)start, (long long)end, (long long)t->n_elems);
         packed_end = end;
-        if (!t->offsets_host && h->uniform && t->batch > 1) {
-            // packed uniform: the last train bounds everything
-            int64_t last;
-            if (!mul_ok(elems, t->batch, &last)) return fail(TTC_ERR_OVERFLOW, "%s: batch size overflows", name);
-            if (t->n_elems > 0 && last > t->n_elems)
-                return fail(TTC_ERR_OVERFLOW, "%s: %d packed trains of %lld floats exceed n_elems = %lld", name,
-                            t->batch, (long long)elems, (long long)t->n_elems);
-            break;
-        }
     }
     return TTC_OK;
 }
@@ -321,16 +339,13 @@ struct ttc_contract_plan {
     bool uniform_out = true;                  // every pair has the same output ranks
     int64_t scratch_floats = 0;               // per-CTA shared scratch for transfers: TL + TR + 3 tmp
     int64_t tl_floats = 0, tr_floats = 0, tmp_floats = 0;
+    // TTCP splice of end modes (ttc_splice_plan_create): chain sources / reversal, K's absorption position
+    bool splice = false;
+    int sn = 0, sm = 0, nx = 0;
+    std::vector<int32_t> sp_src, sp_rev;
+    int64_t k_floats = 1;                     // largest K (Rk x Pk) over the batch
+    bool rows_equal_x = true, rows_equal_y = true;   // every pair has the same rank row (per operand)
 };
-
-namespace {
-
-int64_t core_elems_of(const ttc_contract_plan& p, int b, int l) {
-    const int32_t* r = p.out_ranks.data() + (int64_t)b * (p.L + 1);
-    return (int64_t)r[l] * p.out_dims[l] * r[l + 1];
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -458,6 +473,108 @@ ttc_status ttc_contract_plan_create(const ttc_tt_batch* x, const ttc_tt_batch* y
     if (L > 0 && scratch * (int64_t)sizeof(float) > 200 * 1024)
         return fail(TTC_ERR_UNSUPPORTED, "transfer scratch of %lld floats exceeds shared memory (ranks too large)",
                     (long long)scratch);
+    for (int b = 1; b < p->B && p->rows_equal_x; ++b)
+        p->rows_equal_x = std::equal(p->xranks.begin(), p->xranks.begin() + (p->N + 1), p->xranks.begin() + (size_t)b * (p->N + 1));
+    for (int b = 1; b < p->B && p->rows_equal_y; ++b)
+        p->rows_equal_y = std::equal(p->yranks.begin(), p->yranks.begin() + (p->M + 1), p->yranks.begin() + (size_t)b * (p->M + 1));
+    *plan = p.release();
+    return TTC_OK;
+}
+
+ttc_status ttc_splice_plan_create(const ttc_tt_batch* x, const ttc_tt_batch* y, int32_t x_mode, int32_t y_mode,
+                                  ttc_contract_plan** plan) {
+    g_last_error.clear();
+    if (!plan) return fail(TTC_ERR_NULL, "plan output pointer is NULL");
+    *plan = nullptr;
+    HostTrain hx, hy;
+    ttc_status st;
+    if ((st = check_batch(x, "X", ttc::kMaxContractOrder, &hx)) != TTC_OK) return st;
+    if ((st = check_batch(y, "Y", ttc::kMaxContractOrder, &hy)) != TTC_OK) return st;
+    if (x->batch != y->batch) return fail(TTC_ERR_SHAPE, "batch mismatch: X has %d trains, Y has %d", x->batch, y->batch);
+    const int N = x->order, M = y->order;
+    if (x_mode != 1 && x_mode != N)
+        return fail(TTC_ERR_MODES, "X mode %d is not an end mode (1 or %d): use ttc_contract_plan_create", x_mode, N);
+    if (y_mode != 1 && y_mode != M)
+        return fail(TTC_ERR_MODES, "Y mode %d is not an end mode (1 or %d): use ttc_contract_plan_create", y_mode, M);
+    if (x->dims[x_mode - 1] != y->dims[y_mode - 1])
+        return fail(TTC_ERR_SHAPE, "X mode %d (I=%d) vs Y mode %d (J=%d)", x_mode, x->dims[x_mode - 1], y_mode,
+                    y->dims[y_mode - 1]);
+    std::unique_ptr<ttc_contract_plan> p(new ttc_contract_plan());
+    p->splice = true;
+    p->sn = x_mode; p->sm = y_mode;
+    p->B = x->batch; p->N = N; p->M = M; p->K = 1; p->L = N + M - 2;
+    p->xdims.assign(x->dims, x->dims + N);
+    p->ydims.assign(y->dims, y->dims + M);
+    p->xmodes.assign(1, x_mode);
+    p->ymodes.assign(1, y_mode);
+    // chain (Alg. 2 step 5): X free cores (N..2 reversed when n = 1, else 1..N-1), then Y free cores
+    if (x_mode == 1) for (int k = N; k >= 2; --k) { p->sp_src.push_back(k); p->sp_rev.push_back(1); }
+    else for (int k = 1; k <= N - 1; ++k) { p->sp_src.push_back(k); p->sp_rev.push_back(0); }
+    p->nx = (int)p->sp_src.size();
+    if (y_mode == 1) for (int k = 2; k <= M; ++k) { p->sp_src.push_back(-k); p->sp_rev.push_back(0); }
+    else for (int k = M - 1; k >= 1; --k) { p->sp_src.push_back(-k); p->sp_rev.push_back(1); }
+    const int L = p->L;
+    for (int l = 0; l < L; ++l) {
+        const int sidx = p->sp_src[l];
+        p->out_src.push_back(sidx);
+        p->out_dims.push_back(sidx > 0 ? x->dims[sidx - 1] : y->dims[-sidx - 1]);
+    }
+    for (int n = 1; n <= N; ++n)
+        for (int l = 0; l < L; ++l) if (p->out_src[l] == n) p->out_perm.push_back(l + 1);
+    for (int m = 1; m <= M; ++m)
+        for (int l = 0; l < L; ++l) if (p->out_src[l] == -m) p->out_perm.push_back(l + 1);
+    const int B = p->B;
+    p->xranks.resize((size_t)B * (N + 1));
+    p->yranks.resize((size_t)B * (M + 1));
+    p->out_ranks.assign((size_t)B * (L + 1), 1);
+    p->out_offsets.assign(B, 0);
+    int64_t off = 0;
+    for (int b = 0; b < B; ++b) {
+        for (int n = 0; n <= N; ++n) p->xranks[(size_t)b * (N + 1) + n] = hx.rank(b, n);
+        for (int m = 0; m <= M; ++m) p->yranks[(size_t)b * (M + 1) + m] = hy.rank(b, m);
+        const int32_t* xr = p->xranks.data() + (size_t)b * (N + 1);
+        const int32_t* yr = p->yranks.data() + (size_t)b * (M + 1);
+        const int64_t Rk = x_mode == 1 ? xr[1] : xr[N - 1], Pk = y_mode == 1 ? yr[1] : yr[M - 1];
+        p->k_floats = std::max(p->k_floats, Rk * Pk);
+        int32_t* orr = p->out_ranks.data() + (size_t)b * (L + 1);
+        for (int l = 0; l < L; ++l) {   // right bond of chain core l (its left bond is the previous right bond)
+            const int sidx = p->sp_src[l];
+            const int32_t* rr = sidx > 0 ? xr : yr;
+            const int k = (sidx > 0 ? sidx : -sidx) - 1;
+            orr[l + 1] = p->sp_rev[l] ? rr[k] : rr[k + 1];
+        }
+        orr[0] = 1;
+        if (L > 0) orr[L] = 1;
+        int64_t pair_elems = 0;
+        for (int l = 0; l < L; ++l) {
+            int64_t cl;
+            if (!mul_ok((int64_t)orr[l] * p->out_dims[l], orr[l + 1], &cl) || !add_ok(pair_elems, cl, &pair_elems))
+                return fail(TTC_ERR_OVERFLOW, "pair %d: output train size overflows int64", b);
+            p->max_rank = std::max(p->max_rank, orr[l + 1]);
+        }
+        if (L == 0) pair_elems = 1;
+        p->out_offsets[b] = off;
+        if (!add_ok(off, pair_elems, &off)) return fail(TTC_ERR_OVERFLOW, "total output size overflows int64");
+    }
+    p->total = off;
+    for (int b = 1; b < B && p->uniform_out; ++b)
+        for (int l = 0; l <= L; ++l)
+            if (p->out_ranks[(size_t)b * (L + 1) + l] != p->out_ranks[l]) { p->uniform_out = false; break; }
+    if (p->k_floats * (int64_t)sizeof(float) > 200 * 1024)
+        return fail(TTC_ERR_UNSUPPORTED, "K of %lld floats exceeds shared memory (ranks too large)",
+                    (long long)p->k_floats);
+    for (int b = 0; b < B; ++b)   // the splice kernel indexes a core with 32-bit magic-number divisions
+        for (int l = 0; l < L; ++l) {
+            const int32_t* orr = p->out_ranks.data() + (size_t)b * (L + 1);
+            if ((int64_t)orr[l] * p->out_dims[l] * orr[l + 1] >= (1 << 20) || p->out_dims[l] > 4096)
+                return fail(TTC_ERR_UNSUPPORTED, "pair %d: output core %d of %lld elements (or I = %d) too large "
+                            "for the splice kernel (< 2^20 elements, I <= 4096)", b, l + 1,
+                            (long long)orr[l] * p->out_dims[l] * orr[l + 1], p->out_dims[l]);
+        }
+    for (int b = 1; b < p->B && p->rows_equal_x; ++b)
+        p->rows_equal_x = std::equal(p->xranks.begin(), p->xranks.begin() + (p->N + 1), p->xranks.begin() + (size_t)b * (p->N + 1));
+    for (int b = 1; b < p->B && p->rows_equal_y; ++b)
+        p->rows_equal_y = std::equal(p->yranks.begin(), p->yranks.begin() + (p->M + 1), p->yranks.begin() + (size_t)b * (p->M + 1));
     *plan = p.release();
     return TTC_OK;
 }
@@ -500,14 +617,31 @@ ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const
         if (x->dims[n] != p->xdims[n]) return fail(TTC_ERR_SHAPE, "X mode %d: I=%d differs from the plan (%d)", n + 1, x->dims[n], p->xdims[n]);
     for (int m = 0; m < p->M; ++m)
         if (y->dims[m] != p->ydims[m]) return fail(TTC_ERR_SHAPE, "Y mode %d: J=%d differs from the plan (%d)", m + 1, y->dims[m], p->ydims[m]);
-    for (int b = 0; b < p->B; ++b) {
-        for (int n = 0; n <= p->N; ++n)
-            if (hx.rank(b, n) != p->xranks[(size_t)b * (p->N + 1) + n])
-                return fail(TTC_ERR_SHAPE, "X pair %d: rank R_%d differs from the plan", b, n);
-        for (int m = 0; m <= p->M; ++m)
-            if (hy.rank(b, m) != p->yranks[(size_t)b * (p->M + 1) + m])
-                return fail(TTC_ERR_SHAPE, "Y pair %d: rank P_%d differs from the plan", b, m);
-    }
+    // the operands' ranks must be the plan's (uniform descriptors: compare the rank rows of one pair against
+    // every stored row only when the plan saw different rows; explicit ranks: compare the arrays)
+    auto same_ranks = [&](const HostTrain& h, const std::vector<int32_t>& pr, int n1, const char* nm) -> ttc_status {
+        if (h.uniform) {
+            const bool eq = (nm[0] == 'X') ? p->rows_equal_x : p->rows_equal_y;
+            if (eq && p->B > 0) {   // the plan's rows are all equal: compare one row
+                for (int n = 0; n < n1; ++n)
+                    if (pr[n] != h.rank(0, n)) return fail(TTC_ERR_SHAPE, "%s: rank %d differs from the plan", nm, n);
+                return TTC_OK;
+            }
+            for (int b = 0; b < p->B; ++b)
+                for (int n = 0; n < n1; ++n)
+                    if (pr[(size_t)b * n1 + n] != h.rank(0, n))
+                        return fail(TTC_ERR_SHAPE, "%s pair %d: rank %d differs from the plan", nm, b, n);
+            return TTC_OK;
+        }
+        if (std::memcmp(h.t->ranks_host, pr.data(), sizeof(int32_t) * pr.size()) != 0)
+            for (int b = 0; b < p->B; ++b)
+                for (int n = 0; n < n1; ++n)
+                    if (h.t->ranks_host[(size_t)b * n1 + n] != pr[(size_t)b * n1 + n])
+                        return fail(TTC_ERR_SHAPE, "%s pair %d: rank %d differs from the plan", nm, b, n);
+        return TTC_OK;
+    };
+    if ((st = same_ranks(hx, p->xranks, p->N + 1, "X")) != TTC_OK) return st;
+    if ((st = same_ranks(hy, p->yranks, p->M + 1, "Y")) != TTC_OK) return st;
     if (p->B == 0) return TTC_OK;
     if (!out_cores_dev) return fail(TTC_ERR_NULL, "out_cores_dev is NULL");
     if (reinterpret_cast<uintptr_t>(out_cores_dev) & 3u) return fail(TTC_ERR_ALIGN, "out_cores_dev not 4-byte aligned");
@@ -515,6 +649,22 @@ ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const
         return fail(TTC_ERR_NULL, "pairs have different output ranks: out_offsets_dev is required");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
+    if (p->splice) {   // the paper's TTCP splice of end modes (splice.cu)
+        ttc::SpliceArgs sa;
+        std::memset(&sa, 0, sizeof(sa));
+        sa.B = p->B; sa.N = p->N; sa.M = p->M; sa.L = p->L; sa.n = p->sn; sa.m = p->sm; sa.nx = p->nx;
+        for (int n = 0; n < p->N; ++n) sa.xdims[n] = p->xdims[n];
+        for (int m = 0; m < p->M; ++m) sa.ydims[m] = p->ydims[m];
+        for (int l = 0; l < p->L; ++l) { sa.src[l] = p->sp_src[l]; sa.rev[l] = p->sp_rev[l]; }
+        sa.x = to_dev(hx);
+        sa.y = to_dev(hy);
+        sa.out = out_cores_dev;
+        sa.out_offsets = out_offsets_dev;
+        sa.out_pair_elems = p->B ? p->total / p->B : 0;
+        e = ttc::launch_splice(sa, sizeof(float) * (size_t)p->k_floats, s);
+        if (e != cudaSuccess) return cuda_fail(e, "ttc_contract (splice) launch");
+        return TTC_OK;
+    }
     if (p->L == 0) {   // every mode contracted: the scalar <X_b, Y_b>, one float per pair (packed)
         const ttc_status r = ttc_inner(x, y, out_cores_dev, stream);
         return r;

@@ -79,4 +79,20 @@ struct ContractArgs {
 
 cudaError_t launch_contract(const ContractArgs& a, size_t smem_bytes, cudaStream_t s);
 
+// ---- TTCP splice of end modes (splice.cu) ------------------------------------------------------------
+struct SpliceArgs {
+    int32_t  B, N, M, L;
+    int32_t  n, m;                      // contracted modes, 1-based, n in {1, N}, m in {1, M}
+    int32_t  nx;                        // chain position of the core absorbing K from the left (L: none, right)
+    int32_t  xdims[kMaxContractOrder];
+    int32_t  ydims[kMaxContractOrder];
+    int32_t  src[kMaxLadder];           // +(mode + 1) X, -(mode + 1) Y (0-based mode inside)
+    int32_t  rev[kMaxLadder];           // 1: rank modes swapped
+    TrainDev x, y;
+    float*   out;
+    const int64_t* out_offsets;         // device [B] or nullptr (uniform)
+    int64_t  out_pair_elems;
+};
+cudaError_t launch_splice(const SpliceArgs& a, size_t smem_bytes, cudaStream_t s);
+
 }  // namespace ttc

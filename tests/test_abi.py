@@ -28,7 +28,7 @@ def _declared_symbols():
 
 def test_library_exports_every_declared_symbol():
     syms = _declared_symbols()
-    assert len(syms) == 11
+    assert len(syms) == 12
     lib = ctypes.CDLL(ttc.LIB_PATH)
     for s in syms:
         assert hasattr(lib, s), s
@@ -162,6 +162,50 @@ def test_contract_plan_metadata_matches_oracle_exhaustive():
                 assert plan.total == total
                 n += 1
     assert n > 50
+
+
+def test_splice_plan_metadata_matches_oracle():
+    """Host splice plan (chain order, dims, src, perm, per-pair ranks and sizes) == oracle O5, exactly, for
+    every end-mode choice; interior modes are rejected (TTC_ERR_MODES)."""
+    rng = np.random.default_rng(1)
+    n_cases = 0
+    for N, M in [(1, 1), (1, 3), (2, 2), (3, 3), (4, 2), (5, 4)]:
+        for n in sorted({1, N}):
+            for m in sorted({1, M}):
+                xd = list(rng.integers(1, 4, N))
+                yd = list(rng.integers(1, 4, M))
+                yd[m - 1] = xd[n - 1]
+                B = 3
+                xr = np.stack([[1] + list(rng.integers(1, 5, N - 1)) + [1] for _ in range(B)]).astype(np.int32)
+                yr = np.stack([[1] + list(rng.integers(1, 5, M - 1)) + [1] for _ in range(B)]).astype(np.int32)
+                xo, xt = ttgen.packed_offsets(xr, xd)
+                yo, yt = ttgen.packed_offsets(yr, yd)
+                X = ttc.TTDevice(torch.zeros(xt), xd, ranks=xr, offsets=xo)
+                Y = ttc.TTDevice(torch.zeros(yt), yd, ranks=yr, offsets=yo)
+                plan = ttc.ttc_splice_plan_create(X, Y, n, m)
+                total = 0
+                for b in range(B):
+                    res = oracle.tt_splice(ref.random_train(rng, xd, xr[b]), ref.random_train(rng, yd, yr[b]), n, m,
+                                           with_cores=False)
+                    assert plan.L == res["order"]
+                    assert list(plan.dims) == list(res["dims"])
+                    assert list(plan.src) == list(res["src"])
+                    assert list(plan.perm) == list(res["perm"])
+                    assert list(plan.ranks[b]) == list(res["ranks"])
+                    assert plan.offsets[b] == total
+                    total += res["elems"]
+                assert plan.total == total
+                n_cases += 1
+    assert n_cases == 19
+    x, y = _dev(N=3, dims=(2, 3, 2)), _dev(N=3, dims=(2, 3, 2))
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_splice_plan_create(x, y, 2, 1)
+    assert e.value.status == ttc.TTC_ERR_MODES
+    x2 = _dev(N=3, dims=(3, 3, 2))
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_splice_plan_create(x2, y, 1, 1)         # I_1 = 3 vs J_1 = 2
+    assert e.value.status == ttc.TTC_ERR_SHAPE
+    assert "X mode 1 (I=3) vs Y mode 1 (J=2)" in ttc.ttc_last_error()
 
 
 def test_c3_plan_hand_values():

@@ -32,8 +32,11 @@ CONFIGS = {
     "C3": dict(op="contract", B=1024, N=6, M=6, I=8, R=8, P=8, x_modes=(2, 4, 6), y_modes=(1, 3, 5)),
     "C4": dict(op="inner", B=8192, N=16, I=4, R=64),
     "C5": dict(op="inner", B=65536, N=64, I=2, rank_choices=(8, 16, 24, 32)),
+    # SURVEY.md §8f NEXT-1 (not a BASELINE.json config): the paper's TTCP splice of end modes on C3's operands,
+    # contracting X mode 1 with Y mode 1 (Example 2's x_1^1, on TT operands)
+    "S1": dict(op="splice", B=16384, N=6, M=6, I=8, R=8, P=8, x_mode=1, y_mode=1),
 }
-CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
+CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "S1": 6}
 DEFAULT_SEED = 20210901  # arXiv 2109.00626 submission month; recorded in every bench line
 SIDE_X, SIDE_Y = 0, 1
 
@@ -232,7 +235,7 @@ def config_batch(cfg: str, kind: str = "iid", b0: int = 0, B: Optional[int] = No
         if kind in ("self", "corr"):
             yr = xr
         return make_pair(kind, seed, cid, b0, xr, (c["I"],) * N, yr, rule="geo", device=device)
-    if cfg == "C3":
+    if cfg in ("C3", "S1"):
         xr = uniform_ranks(B, c["N"], c["R"])
         yr = uniform_ranks(B, c["M"], c["P"])
         X = gaussian_batch(seed, cid, SIDE_X, b0, xr, (c["I"],) * c["N"], "uniform", device)
