@@ -65,6 +65,9 @@ def _oracle_pairs(cfg, X, Y, count, nthreads):
         else:
             oracle.tt_contract_batch(X, Y, list(c["x_modes"]), list(c["y_modes"]), offs, per * count, nthreads, 0,
                                      count)
+    elif c["op"] == "reconstruct":   # O1a per train (a plain loop; the oracle has no batch entry for it)
+        for b in range(count):
+            oracle.tt_reconstruct(X.train(b))
     else:
         xc = np.ascontiguousarray(X.cores.detach().cpu().numpy(), dtype=np.float32)
         yc = np.ascontiguousarray(Y.cores.detach().cpu().numpy(), dtype=np.float32)
@@ -73,7 +76,7 @@ def _oracle_pairs(cfg, X, Y, count, nthreads):
 
 def _oracle_name(cfg):
     op = ttgen.CONFIGS[cfg]["op"]
-    return {"contract": "O3", "splice": "O5"}.get(op, "O2")
+    return {"contract": "O3", "splice": "O5", "reconstruct": "O1a"}.get(op, "O2")
 
 
 def per_rank_pairs(cfg: str) -> int:
@@ -243,6 +246,18 @@ def main():
         def step():
             ttc.ttc_contract(plan, XD, YD, out=out, stream=stream)
         kernel_name = "splice_kernel"
+    elif c["op"] == "reconstruct":
+        n_el = c["I"] ** c["N"]
+        out = torch.empty(B * n_el, dtype=torch.float32, device=dev)
+        alg_bytes = 4.0 * X.cores.numel() + 4.0 * out.numel()
+        # left / right partial products (modes 1..N/2, N/2+1..N) and their product, uniform ranks
+        h = c["N"] // 2
+        build = sum(c["I"] ** j * c["R"] * c["R"] for j in range(2, h + 1)) * 2
+        alg_flops = 2.0 * B * (build + n_el * c["R"])
+
+        def step():
+            ttc.ttc_reconstruct(XD, None, out=out, stream=stream)
+        kernel_name = "reconstruct_kernel"
     else:
         out = torch.empty(B, dtype=torch.float32, device=dev)
         mac, byts = ttc.ttc_pair_cost(XD, YD)

@@ -149,6 +149,21 @@ ttc_status ttc_contract(const ttc_contract_plan* plan, const ttc_tt_batch* x, co
 void ttc_contract_plan_destroy(ttc_contract_plan* plan);
 
 /* ---------------------------------------------------------------------------------------------------
+ * ttc_reconstruct: the dense tensor of every train of a batch (Eq. 9: the cores contracted
+ * over consecutive rank modes), written in Eq. 2 order (first index fastest) after an optional
+ * mode permutation -- Alg. 2 steps 5-6 ("obtain reconstructed version of Z^rho", then permute
+ * Z^rho -> Z).  perm: host int32 [N], 1-based, output mode c is the train's mode perm[c] (pass a contraction
+ * plan's out_perm to obtain Eq. 8's order), NULL = identity.  out_dev: device fp32, prod_n I_n floats per train
+ * at out_offsets_dev[b] (device int64 [B]; NULL = packed, train b at b * prod_n I_n).
+ * The kernel splits every train into a left and a right block of modes whose partial products fit in shared
+ * memory together (prod_{n<=k} I_n R_k + R_k prod_{n>k} I_n <= 48K floats for some k) and multiplies them;
+ * trains with no such split return TTC_ERR_UNSUPPORTED.  Errors as ttc_inner (TTC_ERR_MODES for a perm that is
+ * not a permutation of 1..N).
+ * ------------------------------------------------------------------------------------------------- */
+ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
+                           void* stream);
+
+/* ---------------------------------------------------------------------------------------------------
  * Host cost model and batch partitioner (multi-GPU sharding).
  * ttc_pair_cost: per pair b of ttc_inner, mac[b] = sweep MACs (cheaper association per step) and
  *                bytes[b] = algorithmic HBM bytes (every core read once + 4-byte result).  Host only.

@@ -34,7 +34,7 @@ TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG 
 TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
 
 EXPORTED = ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
-            "ttc_contract_plan_layout",
+            "ttc_contract_plan_layout", "ttc_reconstruct",
             "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
             "ttc_last_error", "ttc_version")
 
@@ -64,8 +64,9 @@ _lib.ttc_status_string.restype = ctypes.c_char_p
 _lib.ttc_status_string.argtypes = [ctypes.c_int]
 _lib.ttc_last_error.restype = ctypes.c_char_p
 _lib.ttc_version.restype = ctypes.c_int32
+_lib.ttc_reconstruct.argtypes = [_P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 for _f in ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
-           "ttc_contract_plan_layout",
+           "ttc_contract_plan_layout", "ttc_reconstruct",
            "ttc_contract", "ttc_pair_cost", "ttc_partition"):
     getattr(_lib, _f).restype = ctypes.c_int
 
@@ -276,6 +277,18 @@ def ttc_contract(plan: ContractPlan, x: TTDevice, y: TTDevice, out: torch.Tensor
     _check(_lib.ttc_contract(plan.handle, ctypes.byref(x.c), ctypes.byref(y.c), _ptr(out) if out.numel() else None,
                              _ptr(offs_dev), _stream_handle(stream)))
     return out, plan.ranks, plan.offsets
+
+
+def ttc_reconstruct(t: TTDevice, perm=None, out: torch.Tensor = None, out_offsets=None, stream=None) -> torch.Tensor:
+    """Dense tensor of every train (ttc.h: ttc_reconstruct), Eq. 2 order after the optional mode permutation
+    perm (1-based; e.g. a contraction plan's perm gives Eq. 8's order).  Returns float32 [B * prod(dims)] (packed)."""
+    n_el = int(np.prod(t.dims_np.astype(np.int64))) if t.N else 1
+    if out is None:
+        out = torch.empty(max(t.B * n_el, 0), dtype=torch.float32, device=t.cores.device)
+    pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    _check(_lib.ttc_reconstruct(ctypes.byref(t.c), _ptr(pm), _ptr(out) if out.numel() else None, _ptr(out_offsets),
+                                _stream_handle(stream)))
+    return out
 
 
 def ttc_pair_cost(x: TTDevice, y: TTDevice):

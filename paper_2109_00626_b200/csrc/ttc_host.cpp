@@ -247,6 +247,81 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     return TTC_OK;
 }
 
+ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
+                           void* stream) {
+    g_last_error.clear();
+    HostTrain h;
+    ttc_status st;
+    if ((st = check_batch(t, "T", TTC_MAX_ORDER, &h)) != TTC_OK) return st;
+    const int N = t->order, B = t->batch;
+    // output strides of the train's modes: output mode c is train mode perm[c] (1-based)
+    std::vector<int64_t> ostride(N, 0);
+    {
+        std::vector<int> seen(N, 0);
+        int64_t stride = 1;
+        for (int c = 0; c < N; ++c) {
+            const int m = perm ? perm[c] : c + 1;
+            if (m < 1 || m > N || seen[m - 1])
+                return fail(TTC_ERR_MODES, "perm[%d] = %d: perm must be a permutation of 1..%d", c, m, N);
+            seen[m - 1] = 1;
+            ostride[m - 1] = stride;
+            if (!mul_ok(stride, t->dims[m - 1], &stride)) return fail(TTC_ERR_OVERFLOW, "dense size overflows int64");
+        }
+        if (stride >= (int64_t(1) << 31))
+            return fail(TTC_ERR_UNSUPPORTED, "dense tensor of %lld elements per train (>= 2^31)", (long long)stride);
+    }
+    int64_t pair_elems = 1;
+    for (int n = 0; n < N; ++n) pair_elems *= t->dims[n];
+    if (B == 0) return TTC_OK;
+    if (!out_dev) return fail(TTC_ERR_NULL, "out_dev is NULL");
+    if (reinterpret_cast<uintptr_t>(out_dev) & 3u) return fail(TTC_ERR_ALIGN, "out_dev not 4-byte aligned");
+    // the split k: left block modes 1..k, right block k+1..N; shared memory = both blocks + build temporaries +
+    // the row / column offset tables, the batch maximum over pairs, minimised over k
+    const int64_t kSmemMax = 220 * 1024;
+    int best_k = -1;
+    int64_t best = 0, bl = 0, bt1 = 0, br = 0, bt2 = 0;
+    std::vector<int64_t> pre(N + 1, 1), suf(N + 1, 1);
+    for (int n = 0; n < N; ++n) pre[n + 1] = pre[n] * t->dims[n];
+    for (int n = N - 1; n >= 0; --n) suf[n] = suf[n + 1] * t->dims[n];
+    for (int k = 1; k <= (N == 1 ? 1 : N - 1); ++k) {
+        // the left chain's partial products P_j (pre[j] x R_j, j = 1..k) alternate between Left and its
+        // temporary so that P_k lands in Left; the right chain's Q_j (R_j x suf[j], j = N-1..k) likewise
+        int64_t lb = 0, t1 = 0, rb = N == 1 ? 1 : 0, t2 = 0;
+        for (int b = 0; b < B; ++b) {
+            for (int j = 1; j <= k; ++j) {
+                const int64_t v = pre[j] * h.rank(b, j);
+                if ((k - j) % 2 == 0) lb = std::max(lb, v); else t1 = std::max(t1, v);
+            }
+            for (int j = k; j < N; ++j) {
+                const int64_t v = suf[j] * h.rank(b, j);
+                if ((j - k) % 2 == 0) rb = std::max(rb, v); else t2 = std::max(t2, v);
+            }
+        }
+        auto r4 = [](int64_t v) { return (v + 3) & ~int64_t(3); };   // keep every buffer 16-byte aligned
+        lb = r4(lb); t1 = r4(t1); rb = r4(rb); t2 = r4(t2);
+        const int64_t bytes = 4 * (lb + t1 + rb + t2 + pre[k] + suf[k]);
+        if (bytes <= kSmemMax && (best_k < 0 || bytes < best)) {
+            best_k = k; best = bytes; bl = lb; bt1 = t1; br = rb; bt2 = t2;
+        }
+    }
+    if (best_k < 0)
+        return fail(TTC_ERR_UNSUPPORTED, "no split of the %d modes fits shared memory (partial products too large)", N);
+    ttc::ReconArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.B = B; a.N = N; a.k = best_k;
+    a.rows = (int32_t)pre[best_k];
+    a.cols = (int32_t)suf[best_k];
+    a.lbuf = (int32_t)bl; a.t1 = (int32_t)bt1; a.rbuf = (int32_t)br; a.t2 = (int32_t)bt2;
+    for (int n = 0; n < N; ++n) { a.dims[n] = t->dims[n]; a.ostride[n] = ostride[n]; }
+    a.t = to_dev(h);
+    a.out = out_dev;
+    a.out_offsets = out_offsets_dev;
+    a.pair_elems = pair_elems;
+    const cudaError_t e = ttc::launch_reconstruct(a, (size_t)best, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "ttc_reconstruct launch");
+    return TTC_OK;
+}
+
 ttc_status ttc_pair_cost(const ttc_tt_batch* x, const ttc_tt_batch* y, double* mac, double* bytes) {
     g_last_error.clear();
     HostTrain hx, hy;

@@ -95,4 +95,18 @@ struct SpliceArgs {
 };
 cudaError_t launch_splice(const SpliceArgs& a, size_t smem_bytes, cudaStream_t s);
 
+// ---- dense reconstruction (reconstruct.cu) -------------------------------------------------------------
+struct ReconArgs {
+    int32_t  B, N, k;                   // split: left block = modes 1..k, right block = k+1..N (1 <= k < N)
+    int32_t  rows, cols;                // prod_{n<=k} I_n, prod_{n>k} I_n
+    int32_t  lbuf, t1, rbuf, t2;        // floats of: Left (+ same-parity partials), its temporary, Right, its temporary
+    int32_t  dims[TTC_MAX_ORDER];
+    int64_t  ostride[TTC_MAX_ORDER];    // output stride of train mode n (permuted Eq. 2 order)
+    TrainDev t;
+    float*   out;
+    const int64_t* out_offsets;         // device [B] or nullptr (packed)
+    int64_t  pair_elems;                // prod_n I_n
+};
+cudaError_t launch_reconstruct(const ReconArgs& a, size_t smem_bytes, cudaStream_t s);
+
 }  // namespace ttc

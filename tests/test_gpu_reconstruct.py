@@ -1,0 +1,116 @@
+"""GPU parity for ttc_reconstruct (dense tensors of trains, Alg. 2 steps 5-6) against the
+oracle's Eq. 9 reconstruction (O1a, pinned in test_oracle_dense.py) and numpy's transpose for the permutation;
+end to end, contraction / splice on the GPU followed by reconstruction equals the dense Eq. 8 definition."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2109_00626_b200 as ttc
+import ttgen
+from tests import ref_numpy as ref
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _recon(T, perm=None):
+    TD = ttc.TTDevice.from_batch(T, DEV)
+    out = ttc.ttc_reconstruct(TD, perm)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+def _want(cores, perm):
+    d = oracle.tt_reconstruct(cores)
+    return d if perm is None else np.transpose(d, [p - 1 for p in perm])
+
+
+def _check(T, got, perm=None, tol=2e-6):
+    n_el = int(np.prod(T.dims))
+    for b in range(T.B):
+        cores = T.train(b)
+        want = _want(cores, perm)
+        seg = got[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
+        # fp32 sums of R_k products: bound by the reconstruction of |cores| (the exact sum of |terms|)
+        bound = oracle.tt_reconstruct([np.abs(c) for c in cores])
+        if perm is not None:
+            bound = np.transpose(bound, [p - 1 for p in perm])
+        assert np.max(np.abs(seg - want) / np.maximum(bound, 1e-30)) <= tol, f"train {b}"
+
+
+@pytest.mark.parametrize("case", range(7))
+def test_random_trains(case):
+    """Orders 1..6, odd mode sizes, heterogeneous per-train ranks, with and without a permutation."""
+    rng = np.random.default_rng(40 + case)
+    dims = [(7,), (3, 5), (4, 1, 6), (2, 3, 4, 5), (5, 4, 3, 2, 3), (3, 2, 3, 2, 3, 2), (20, 20, 20, 20)][case]
+    N = len(dims)
+    B = 5
+    r = np.stack([[1] + list(rng.integers(1, 9, N - 1)) + [1] for _ in range(B)]).astype(np.int32)
+    T = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, r, dims, "geo")
+    _check(T, _recon(T))
+    perm = list(rng.permutation(N) + 1)
+    _check(T, _recon(T, perm), perm)
+
+
+def test_r1_sampled_and_uniform():
+    """The R1 workload bench.py --config R1 times (Example 2's TTCP output, order 4, I = 20, ranks 20)."""
+    T, _ = ttgen.config_batch("R1", B=64)
+    got = _recon(T)
+    n_el = 20 ** 4
+    for b in (0, 63):
+        want = oracle.tt_reconstruct(T.train(b))
+        seg = got[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
+        bound = oracle.tt_reconstruct([np.abs(c) for c in T.train(b)])
+        assert np.max(np.abs(seg - want) / bound) <= 2e-6
+
+
+def test_contract_then_reconstruct_is_eq8():
+    """Alg. 2 steps 4-6 end to end on the GPU: ladder contraction (C3's mode pairs on smaller operands), then the
+    dense reconstruction in Eq. 8 order (perm = the plan's out_perm) == tensordot of the dense operands."""
+    rng = np.random.default_rng(5)
+    dims, xm, ym = (3,) * 6, [2, 4, 6], [1, 3, 5]
+    B = 3
+    r = np.tile(np.array([1, 3, 3, 3, 3, 3, 1], np.int32), (B, 1))
+    X = ttgen.gaussian_batch(11, 0, 0, 0, r, dims, "geo")
+    Y = ttgen.gaussian_batch(12, 0, 1, 0, r, dims, "geo")
+    XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+    plan = ttc.ttc_contract_plan_create(XD, YD, xm, ym)
+    cores, ranks, offs = ttc.ttc_contract(plan, XD, YD)
+    Z = ttc.TTDevice(cores, plan.dims, ranks=ranks, offsets=offs)
+    dense = ttc.ttc_reconstruct(Z, plan.perm).cpu().numpy().astype(np.float64)
+    n_el = 3 ** 6
+    for b in range(B):
+        want = ref.tcp(ref.dense_from_tt(X.train(b)), ref.dense_from_tt(Y.train(b)), xm, ym)
+        got = dense[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
+        err = np.linalg.norm(got - want) / oracle.normaliser(X.train(b), Y.train(b))
+        assert err <= 1e-5
+
+
+def test_splice_then_reconstruct_is_eq8():
+    """The paper's own pipeline on TT operands: splice x_1^1 (Alg. 2 steps 4-5), reconstruct + permute (steps
+    5-6) == Eq. 8 (Example 2's shape: two order-3 tensors, 20 x 20 x 20, TT ranks 6)."""
+    dims = (20, 20, 20)
+    B = 2
+    r = np.tile(np.array([1, 6, 6, 1], np.int32), (B, 1))
+    X = ttgen.gaussian_batch(13, 0, 0, 0, r, dims, "geo")
+    Y = ttgen.gaussian_batch(14, 0, 1, 0, r, dims, "geo")
+    XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+    plan = ttc.ttc_splice_plan_create(XD, YD, 1, 1)
+    cores, ranks, offs = ttc.ttc_contract(plan, XD, YD)
+    Z = ttc.TTDevice(cores, plan.dims, ranks=ranks, offsets=offs)
+    dense = ttc.ttc_reconstruct(Z, plan.perm).cpu().numpy().astype(np.float64)
+    n_el = 20 ** 4
+    for b in range(B):
+        want = ref.tcp(ref.dense_from_tt(X.train(b)), ref.dense_from_tt(Y.train(b)), [1], [1])
+        got = dense[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
+        err = np.linalg.norm(got - want) / oracle.normaliser(X.train(b), Y.train(b))
+        assert err <= 1e-5
+
+
+def test_reconstruct_errors():
+    T, _ = ttgen.config_batch("R1", B=2)
+    TD = ttc.TTDevice.from_batch(T, DEV)
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_reconstruct(TD, [1, 1, 2, 3])
+    assert e.value.status == ttc.TTC_ERR_MODES

@@ -35,8 +35,12 @@ CONFIGS = {
     # SURVEY.md §8f NEXT-1 (not a BASELINE.json config): the paper's TTCP splice of end modes on C3's operands,
     # contracting X mode 1 with Y mode 1 (Example 2's x_1^1, on TT operands)
     "S1": dict(op="splice", B=16384, N=6, M=6, I=8, R=8, P=8, x_mode=1, y_mode=1),
+    # SURVEY.md §8f NEXT-2 (not a BASELINE.json config): dense reconstruction (Alg. 2 steps 5-6) of Example 2's
+    # TTCP output -- x_1^1 of two 20 x 20 x 20 tensors in TT format with ranks 20 is an order-4 train with
+    # I = 20 and bonds 20 -- 160,000 floats per train
+    "R1": dict(op="reconstruct", B=1024, N=4, I=20, R=20),
 }
-CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "S1": 6}
+CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "S1": 6, "R1": 7}
 DEFAULT_SEED = 20210901  # arXiv 2109.00626 submission month; recorded in every bench line
 SIDE_X, SIDE_Y = 0, 1
 
