@@ -164,6 +164,25 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
                            void* stream);
 
 /* ---------------------------------------------------------------------------------------------------
+ * ttc_tt_svd: TT decomposition of a batch of dense tensors (Alg. 1, TT-SVD), optionally of the
+ * permuted tensors X^rho (Alg. 2 step 1): the decomposed tensor's mode k is the input's mode
+ * perm[k] (1-based; NULL = identity).  delta = eps / sqrt(N - 1) ||X||_F; each delta-truncated SVD keeps the
+ * smallest rank with sum of discarded s_j^2 <= delta^2 (R23), singular values below 1e-7 of the largest
+ * count as zero (R25), every left singular vector has its largest-magnitude entry positive (R24); then
+ * ||X - TT(X)||_F <= eps ||X||_F.
+ *   order, dims (host [N]): the INPUT tensor's shape; dense_dev: B tensors of prod(dims) floats, Eq. 2 order,
+ *   packed.  Output: train b is packed (TTD1 layout) from cores_dev + b * train_cap, where train_cap comes from
+ *   ttc_tt_svd_capacity (the floats of the largest possible ranks R_n <= min(prod_{k<=n} I_k, prod_{k>n} I_k));
+ *   ranks_dev: device int32 [B, N + 1], the ranks found (read them back before describing the trains in a
+ *   ttc_tt_batch with offsets b * train_cap).
+ * One CTA per tensor holds the tensor in shared memory: prod(dims) <= 16384 and every unfolding's smaller side
+ * <= 64 (else TTC_ERR_UNSUPPORTED).  eps < 0: TTC_ERR_ARG.
+ * ------------------------------------------------------------------------------------------------- */
+ttc_status ttc_tt_svd_capacity(int32_t order, const int32_t* dims, const int32_t* perm, int64_t* train_cap);
+ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const float* dense_dev, const int32_t* perm,
+                      double eps, float* cores_dev, int32_t* ranks_dev, void* stream);
+
+/* ---------------------------------------------------------------------------------------------------
  * Host cost model and batch partitioner (multi-GPU sharding).
  * ttc_pair_cost: per pair b of ttc_inner, mac[b] = sweep MACs (cheaper association per step) and
  *                bytes[b] = algorithmic HBM bytes (every core read once + 4-byte result).  Host only.

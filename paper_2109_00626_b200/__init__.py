@@ -34,7 +34,7 @@ TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG 
 TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
 
 EXPORTED = ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
-            "ttc_contract_plan_layout", "ttc_reconstruct",
+            "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity", "ttc_tt_svd", "ttc_tt_svd_capacity",
             "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
             "ttc_last_error", "ttc_version")
 
@@ -65,8 +65,11 @@ _lib.ttc_status_string.argtypes = [ctypes.c_int]
 _lib.ttc_last_error.restype = ctypes.c_char_p
 _lib.ttc_version.restype = ctypes.c_int32
 _lib.ttc_reconstruct.argtypes = [_P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_tt_svd_capacity.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_tt_svd.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 for _f in ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
-           "ttc_contract_plan_layout", "ttc_reconstruct",
+           "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity",
            "ttc_contract", "ttc_pair_cost", "ttc_partition"):
     getattr(_lib, _f).restype = ctypes.c_int
 
@@ -289,6 +292,32 @@ def ttc_reconstruct(t: TTDevice, perm=None, out: torch.Tensor = None, out_offset
     _check(_lib.ttc_reconstruct(ctypes.byref(t.c), _ptr(pm), _ptr(out) if out.numel() else None, _ptr(out_offsets),
                                 _stream_handle(stream)))
     return out
+
+
+def ttc_tt_svd_capacity(dims, perm=None) -> int:
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
+    pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    cap = ctypes.c_int64(0)
+    _check(_lib.ttc_tt_svd_capacity(int(d.size), _ptr(d), _ptr(pm), ctypes.byref(cap)))
+    return cap.value
+
+
+def ttc_tt_svd(dense: torch.Tensor, dims, eps: float, perm=None, stream=None) -> "TTDevice":
+    """TT-SVD of B dense tensors (ttc.h: ttc_tt_svd; Alg. 1, optionally of the permuted X^rho of Alg. 2 step 1).
+    dense: float32 [B * prod(dims)] on the device.  Returns the trains as a TTDevice (ranks read back to the host,
+    trains at b * capacity)."""
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
+    pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    n_el = int(np.prod(d.astype(np.int64)))
+    B = dense.numel() // max(n_el, 1)
+    cap = ttc_tt_svd_capacity(d, pm)
+    cores = torch.zeros(max(B * cap, 1), dtype=torch.float32, device=dense.device)
+    ranks = torch.zeros((max(B, 1), d.size + 1), dtype=torch.int32, device=dense.device)
+    _check(_lib.ttc_tt_svd(int(B), int(d.size), _ptr(d), _ptr(dense) if dense.numel() else None, _ptr(pm),
+                           float(eps), _ptr(cores), _ptr(ranks), _stream_handle(stream)))
+    rdims = d if pm is None else d[pm - 1]
+    r = ranks[:B].cpu().numpy()
+    return TTDevice(cores, rdims, ranks=r, offsets=np.arange(B, dtype=np.int64) * cap)
 
 
 def ttc_pair_cost(x: TTDevice, y: TTDevice):

@@ -322,6 +322,97 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
     return TTC_OK;
 }
 
+namespace {
+
+// dims of X^rho and the source strides of its modes; the rank bounds and the capacity of one train
+ttc_status ttsvd_shape(int32_t order, const int32_t* dims, const int32_t* perm, std::vector<int32_t>* rd,
+                       std::vector<int64_t>* stride, int64_t* cap, int32_t* gmax) {
+    if (order < 1 || order > TTC_MAX_ORDER) return fail(TTC_ERR_SHAPE, "order N = %d outside [1, %d]", order, TTC_MAX_ORDER);
+    if (!dims) return fail(TTC_ERR_NULL, "dims is NULL");
+    std::vector<int64_t> xs(order, 1);
+    for (int n = 0; n < order; ++n) {
+        if (dims[n] < 1) return fail(TTC_ERR_SHAPE, "mode %d has I = %d < 1", n + 1, dims[n]);
+        if (n > 0) xs[n] = xs[n - 1] * dims[n - 1];
+        if (xs[n] > (int64_t(1) << 40)) return fail(TTC_ERR_OVERFLOW, "dense size overflows");
+    }
+    rd->assign(order, 0);
+    stride->assign(order, 0);
+    std::vector<int> seen(order, 0);
+    for (int k = 0; k < order; ++k) {
+        const int m = perm ? perm[k] : k + 1;
+        if (m < 1 || m > order || seen[m - 1])
+            return fail(TTC_ERR_MODES, "perm[%d] = %d: perm must be a permutation of 1..%d", k, m, order);
+        seen[m - 1] = 1;
+        (*rd)[k] = dims[m - 1];
+        (*stride)[k] = xs[m - 1];
+    }
+    int64_t total = 1;
+    for (int k = 0; k < order; ++k) total *= (*rd)[k];
+    // capacity: R_n <= min(prod_{k<=n} I_k, prod_{k>n} I_k); the Gram side of step n <= min(R_{n-1} I_n, rest)
+    int64_t c = 0, left = 1, g = 1;
+    int64_t Rprev = 1;
+    for (int n = 0; n < order; ++n) {
+        left *= (*rd)[n];
+        const int64_t right = total / left;
+        const int64_t Rn = n == order - 1 ? 1 : std::min(left, right);
+        c += Rprev * (*rd)[n] * Rn;
+        if (n < order - 1) g = std::max(g, std::min(Rprev * (*rd)[n], right));
+        Rprev = Rn;
+    }
+    *cap = c;
+    *gmax = (int32_t)g;
+    if (total > 16384)
+        return fail(TTC_ERR_UNSUPPORTED, "tensor of %lld elements: the TT-SVD kernel holds <= 16384 in shared memory",
+                    (long long)total);
+    if (g > 64) return fail(TTC_ERR_UNSUPPORTED, "an unfolding's smaller side is %lld > 64", (long long)g);
+    return TTC_OK;
+}
+
+}  // namespace
+
+ttc_status ttc_tt_svd_capacity(int32_t order, const int32_t* dims, const int32_t* perm, int64_t* train_cap) {
+    g_last_error.clear();
+    if (!train_cap) return fail(TTC_ERR_NULL, "train_cap is NULL");
+    std::vector<int32_t> rd;
+    std::vector<int64_t> st;
+    int32_t g;
+    return ttsvd_shape(order, dims, perm, &rd, &st, train_cap, &g);
+}
+
+ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const float* dense_dev, const int32_t* perm,
+                      double eps, float* cores_dev, int32_t* ranks_dev, void* stream) {
+    g_last_error.clear();
+    if (batch < 0) return fail(TTC_ERR_ARG, "batch = %d < 0", batch);
+    if (!(eps >= 0.0)) return fail(TTC_ERR_ARG, "eps = %g must be >= 0", eps);
+    std::vector<int32_t> rd;
+    std::vector<int64_t> st;
+    int64_t cap;
+    int32_t gmax;
+    ttc_status s;
+    if ((s = ttsvd_shape(order, dims, perm, &rd, &st, &cap, &gmax)) != TTC_OK) return s;
+    if (batch == 0) return TTC_OK;
+    if (!dense_dev || !cores_dev || !ranks_dev) return fail(TTC_ERR_NULL, "dense_dev / cores_dev / ranks_dev is NULL");
+    if ((reinterpret_cast<uintptr_t>(dense_dev) | reinterpret_cast<uintptr_t>(cores_dev)) & 3u)
+        return fail(TTC_ERR_ALIGN, "dense_dev / cores_dev not 4-byte aligned");
+    ttc::TtsvdArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.B = batch; a.N = order; a.gmax = gmax;
+    int64_t total = 1;
+    for (int n = 0; n < order; ++n) { a.dims[n] = rd[n]; a.in_stride[n] = st[n]; total *= rd[n]; }
+    a.elems = (int32_t)total;
+    a.dense = dense_dev;
+    a.eps2 = order > 1 ? eps * eps / (order - 1) : 0.0;
+    a.cores = cores_dev;
+    a.train_cap = cap;
+    a.ranks = ranks_dev;
+    const int64_t g = gmax;
+    const size_t smem = sizeof(double) * (size_t)(2 * g * g + g + 2 * (g / 2 + 1) + 32) +
+                        sizeof(int) * (size_t)(g + 2 * (g / 2 + 1) + 4) + 16 + sizeof(float) * 2 * (size_t)total;
+    const cudaError_t e = ttc::launch_ttsvd(a, smem, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd launch");
+    return TTC_OK;
+}
+
 ttc_status ttc_pair_cost(const ttc_tt_batch* x, const ttc_tt_batch* y, double* mac, double* bytes) {
     g_last_error.clear();
     HostTrain hx, hy;

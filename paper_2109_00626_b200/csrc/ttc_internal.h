@@ -109,4 +109,17 @@ struct ReconArgs {
 };
 cudaError_t launch_reconstruct(const ReconArgs& a, size_t smem_bytes, cudaStream_t s);
 
+// ---- batched TT-SVD (ttsvd.cu) -------------------------------------------------------------------------
+struct TtsvdArgs {
+    int32_t  B, N, elems, gmax;         // tensors, order, prod dims (<= shared memory), largest Gram side
+    int32_t  dims[TTC_MAX_ORDER];       // dims of the decomposed tensor X^rho
+    int64_t  in_stride[TTC_MAX_ORDER];  // source stride of X^rho's mode k (Alg. 2 step 1's permutation)
+    const float* dense;                 // B tensors, elems floats each, Eq. 2 order of X
+    double   eps2;                      // eps^2 / (N - 1)
+    float*   cores;                     // B * train_cap floats
+    int64_t  train_cap;
+    int32_t* ranks;                     // device [B, N + 1]
+};
+cudaError_t launch_ttsvd(const TtsvdArgs& a, size_t smem_bytes, cudaStream_t s);
+
 }  // namespace ttc

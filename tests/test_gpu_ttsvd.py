@@ -1,0 +1,124 @@
+"""GPU parity for the batched TT-SVD (ttc_tt_svd; Alg. 1) against oracle O6, and the whole dense-input TTCP
+pipeline of Alg. 2 on the GPU (TT-SVD of X^rho and Y^rho, splice, reconstruction + permutation) against Eq. 8
+(SURVEY.md §8f NEXT-3)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2109_00626_b200 as ttc
+from oracle import ttsvd
+from tests import ref_numpy as ref
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _dense_batch(Xs):
+    return torch.from_numpy(np.concatenate([x.reshape(-1, order="F") for x in Xs]).astype(np.float32)).to(DEV)
+
+
+def _trains(T):
+    cores = T.cores.cpu().numpy().astype(np.float64)
+    out = []
+    rows = T.rank_rows()
+    offs = T.offsets_np if T.offsets_np is not None else T._packed_offsets()
+    for b in range(T.B):
+        r = rows[b]
+        pos, cs = int(offs[b]), []
+        for n in range(T.N):
+            a, i, c = int(r[n]), int(T.dims_np[n]), int(r[n + 1])
+            cs.append(cores[pos:pos + a * i * c].reshape((a, i, c), order="F"))
+            pos += a * i * c
+        out.append(cs)
+    return out
+
+
+@pytest.mark.parametrize("dims", [(5,), (4, 6), (3, 4, 5), (20, 20, 20), (2, 3, 4, 3, 2), (6, 1, 5), (8, 8, 8, 8)])
+def test_full_rank_reconstruction_and_ranks(dims):
+    rng = np.random.default_rng(sum(dims))
+    Xs = [rng.standard_normal(dims) for _ in range(3)]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 0.0)
+    for b, cs in enumerate(_trains(T)):
+        want_cores = ttsvd.tt_svd(Xs[b], 0.0)
+        assert [c.shape for c in cs] == [c.shape for c in want_cores]
+        err = np.linalg.norm(ref.dense_from_tt(cs) - Xs[b]) / np.linalg.norm(Xs[b])
+        assert err <= 2e-5, f"tensor {b}: relative reconstruction error {err:.3e}"
+        for c in cs[:-1]:   # left-orthonormal cores
+            U = c.reshape(-1, c.shape[2], order="F")
+            np.testing.assert_allclose(U.T @ U, np.eye(U.shape[1]), atol=1e-4)
+
+
+def test_low_rank_ranks_and_cores_match_oracle():
+    """A tensor built from a generic low-rank train (well separated singular values): the eps-truncation finds
+    the construction's ranks, and the cores agree with O6 entry by entry (same sign convention, R24)."""
+    rng = np.random.default_rng(3)
+    dims, ranks = (6, 5, 7, 4), [1, 3, 4, 2, 1]
+    Xs = [ref.dense_from_tt(ref.random_train(rng, dims, ranks)) for _ in range(4)]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 1e-5)
+    for b, cs in enumerate(_trains(T)):
+        want = ttsvd.tt_svd(Xs[b], 1e-5)
+        assert [c.shape[0] for c in cs] + [1] == ranks
+        for c, w in zip(cs, want):
+            assert np.max(np.abs(c - w)) <= 1e-3 * np.max(np.abs(w)), "core mismatch"
+
+
+@pytest.mark.parametrize("eps", [0.05, 0.2, 0.5])
+def test_error_guarantee(eps):
+    rng = np.random.default_rng(int(100 * eps))
+    dims = (6, 7, 5, 4)
+    Xs = [rng.standard_normal(dims) for _ in range(4)]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, eps)
+    for b, cs in enumerate(_trains(T)):
+        err = np.linalg.norm(ref.dense_from_tt(cs) - Xs[b])
+        assert err <= eps * np.linalg.norm(Xs[b]) * (1 + 1e-4)
+        # same ranks as the oracle (random spectra: decisions far from the threshold are robust; allow a
+        # difference of one only where the discarded energy is within 1e-4 of delta^2)
+        want = ttsvd.tt_svd(Xs[b], eps)
+        assert all(abs(c.shape[2] - w.shape[2]) <= 1 for c, w in zip(cs[:-1], want[:-1]))
+
+
+def test_permuted_decomposition():
+    """perm (Alg. 2 step 1): the TT of X^rho equals the TT-SVD of numpy's transpose."""
+    rng = np.random.default_rng(9)
+    dims, perm = (4, 5, 6), [3, 1, 2]
+    Xs = [rng.standard_normal(dims) for _ in range(2)]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 0.0, perm=perm)
+    for b, cs in enumerate(_trains(T)):
+        want = np.transpose(Xs[b], [p - 1 for p in perm])
+        np.testing.assert_allclose(ref.dense_from_tt(cs), want, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("shape_x,shape_y,n,m", [((20, 20, 20), (20, 20, 20), 1, 1), ((4, 5, 6), (6, 3), 3, 1),
+                                                 ((3, 4), (5, 4, 2), 2, 2), ((4, 3, 5, 2), (2, 5, 3), 3, 2)])
+def test_alg2_pipeline_on_gpu(shape_x, shape_y, n, m):
+    """Alg. 2 end to end on the GPU == Eq. 8 (Example 2's x_1^1 on 20 x 20 x 20 included), eps = 0."""
+    rng = np.random.default_rng(sum(shape_x) + m)
+    B = 2
+    Xs = [rng.standard_normal(shape_x) for _ in range(B)]
+    Ys = [rng.standard_normal(shape_y) for _ in range(B)]
+    px = [n] + [k for k in range(1, len(shape_x) + 1) if k != n]
+    py = [m] + [k for k in range(1, len(shape_y) + 1) if k != m]
+    TX = ttc.ttc_tt_svd(_dense_batch(Xs), shape_x, 0.0, perm=px)
+    TY = ttc.ttc_tt_svd(_dense_batch(Ys), shape_y, 0.0, perm=py)
+    plan = ttc.ttc_splice_plan_create(TX, TY, 1, 1)
+    cores, ranks, offs = ttc.ttc_contract(plan, TX, TY)
+    Z = ttc.TTDevice(cores, plan.dims, ranks=ranks, offsets=offs)
+    dense = ttc.ttc_reconstruct(Z, plan.perm).cpu().numpy().astype(np.float64)
+    n_el = int(np.prod([d for k, d in enumerate(shape_x) if k != n - 1])) * \
+        int(np.prod([d for k, d in enumerate(shape_y) if k != m - 1]))
+    for b in range(B):
+        want = ref.tcp(Xs[b], Ys[b], [n], [m])
+        got = dense[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
+        err = np.linalg.norm(got - want) / (np.linalg.norm(Xs[b]) * np.linalg.norm(Ys[b]))
+        assert err <= 1e-5, f"pair {b}: {err:.3e}"
+        np.testing.assert_allclose(got, ttsvd.ttcp_dense(Xs[b], Ys[b], n, m, 0.0), rtol=1e-3, atol=1e-3)
+
+
+def test_ttsvd_errors():
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_tt_svd_capacity((30, 30, 30))           # 27,000 elements > 16,384
+    assert e.value.status == ttc.TTC_ERR_UNSUPPORTED
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_tt_svd_capacity((4, 5), perm=[1, 1])
+    assert e.value.status == ttc.TTC_ERR_MODES
