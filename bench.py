@@ -65,6 +65,14 @@ def _oracle_pairs(cfg, X, Y, count, nthreads):
         else:
             oracle.tt_contract_batch(X, Y, list(c["x_modes"]), list(c["y_modes"]), offs, per * count, nthreads, 0,
                                      count)
+    elif c["op"] == "alg2":          # O6: the dense-input TTCP pipeline per pair (numpy)
+        from oracle import ttsvd
+        n_el = c["I"] ** c["N"]
+        shape = (c["I"],) * c["N"]
+        xh, yh = X.cpu().numpy(), Y.cpu().numpy()
+        for b in range(count):
+            ttsvd.ttcp_dense(xh[b * n_el:(b + 1) * n_el].reshape(shape, order="F"),
+                             yh[b * n_el:(b + 1) * n_el].reshape(shape, order="F"), c["x_mode"], c["y_mode"], c["eps"])
     elif c["op"] == "reconstruct":   # O1a per train (a plain loop; the oracle has no batch entry for it)
         for b in range(count):
             oracle.tt_reconstruct(X.train(b))
@@ -76,7 +84,7 @@ def _oracle_pairs(cfg, X, Y, count, nthreads):
 
 def _oracle_name(cfg):
     op = ttgen.CONFIGS[cfg]["op"]
-    return {"contract": "O3", "splice": "O5", "reconstruct": "O1a"}.get(op, "O2")
+    return {"contract": "O3", "splice": "O5", "reconstruct": "O1a", "alg2": "O6"}.get(op, "O2")
 
 
 def per_rank_pairs(cfg: str) -> int:
@@ -154,16 +162,17 @@ def cpu_oracle_rate(cfg: str, X, Y, target_s: float):
         _oracle_pairs(cfg, X, Y, count, nthreads)
         return time.perf_counter() - t0
 
-    probe = max(1, min(X.B, nthreads))
+    nb = X.B if hasattr(X, "B") else X.numel() // (ttgen.CONFIGS[cfg]["I"] ** ttgen.CONFIGS[cfg]["N"])
+    probe = max(1, min(nb, nthreads))
     t = run(probe)
-    count = int(min(X.B, max(probe, probe * target_s / max(t, 1e-6))))
+    count = int(min(nb, max(probe, probe * target_s / max(t, 1e-6))))
     # whole passes over the sample until about target_s of CPU work (the batch may take well under target_s)
     reps, t = 0, 0.0
     while reps == 0 or (t < target_s and reps < 1000):
         t += run(count)
         reps += 1
     return {"value": reps * count / t, "unit": UNIT, "cores": nthreads, "kind": "oracle",
-            "sample": f"{reps} pass(es) over the first {count} of the rank's {X.B} {cfg} pairs (fp64 oracle "
+            "sample": f"{reps} pass(es) over the first {count} of the rank's {nb} {cfg} pairs (fp64 oracle "
                       f"{_oracle_name(cfg)}, OpenMP over pairs), {t:.1f} s"}, count, t / reps
 
 
@@ -173,7 +182,10 @@ def run_reference(args, rank, world):
         return
     cfg = args.config
     B = args.pairs or per_rank_pairs(cfg)
-    X, Y = ttgen.config_batch(cfg, "iid", 0, B, args.seed, "cpu")
+    if ttgen.CONFIGS[cfg]["op"] == "alg2":
+        X, Y = ttgen.dense_pairs(cfg, 0, B, args.seed, "cpu")
+    else:
+        X, Y = ttgen.config_batch(cfg, "iid", 0, B, args.seed, "cpu")
     steps_budget = 150.0 / max(1, args.steps + args.warmup)
     cb, count, t = cpu_oracle_rate(cfg, X, Y, min(args.cpu_seconds, steps_budget))
     times = []
@@ -222,8 +234,12 @@ def main():
     c = ttgen.CONFIGS[cfg]
     B = args.pairs or per_rank_pairs(cfg)
     b0 = rank * B
-    X, Y = ttgen.config_batch(cfg, "iid", b0, B, args.seed, dev)
-    XD, YD = ttc.TTDevice.from_batch(X), ttc.TTDevice.from_batch(Y)
+    if c["op"] == "alg2":
+        X, Y = ttgen.dense_pairs(cfg, b0, B, args.seed, dev)
+        XD = YD = None
+    else:
+        X, Y = ttgen.config_batch(cfg, "iid", b0, B, args.seed, dev)
+        XD, YD = ttc.TTDevice.from_batch(X), ttc.TTDevice.from_batch(Y)
     stream = torch.cuda.current_stream(dev)
 
     if cfg == "C3":
@@ -246,6 +262,37 @@ def main():
         def step():
             ttc.ttc_contract(plan, XD, YD, out=out, stream=stream)
         kernel_name = "splice_kernel"
+    elif c["op"] == "alg2":
+        # Alg. 2 on dense operands: TT-SVD of X^rho and Y^rho (step 1's permutation folded into the read),
+        # K and the splice (steps 4-5), dense reconstruction in Eq. 8 order (steps 5-6)
+        shape = (c["I"],) * c["N"]
+        px = [c["x_mode"]] + [k for k in range(1, c["N"] + 1) if k != c["x_mode"]]
+        py = [c["y_mode"]] + [k for k in range(1, c["N"] + 1) if k != c["y_mode"]]
+        TX = ttc.ttc_tt_svd(X, shape, c["eps"], perm=px)
+        TY = ttc.ttc_tt_svd(Y, shape, c["eps"], perm=py)
+        plan = ttc.ttc_splice_plan_create(TX, TY, 1, 1)
+        rx_dev = torch.from_numpy(TX.rank_rows()).to(dev)
+        ry_dev = torch.from_numpy(TY.rank_rows()).to(dev)
+        zc = torch.empty(plan.total, dtype=torch.float32, device=dev)
+        ZD = ttc.TTDevice(zc, plan.dims, ranks=plan.ranks, offsets=plan.offsets)
+        n_out = int(np.prod(plan.dims.astype(np.int64)))
+        out = torch.empty(B * n_out, dtype=torch.float32, device=dev)
+        rk_x = torch.empty_like(rx_dev)
+        rk_y = torch.empty_like(ry_dev)
+        n_in = c["I"] ** c["N"]
+        train_x = int(sum(int(a) * int(i) * int(b2) for a, i, b2 in
+                          zip(TX.rank_rows()[0][:-1], TX.dims_np, TX.rank_rows()[0][1:])))
+        alg_bytes = 4.0 * B * (2 * n_in + 2 * 2 * train_x + 2 * (plan.total // B) + n_out)
+        R1, I = int(TX.rank_rows()[0][1]), c["I"]
+        svd_mac = 2 * (I * I * n_in // I + 2 * I ** 3 * R1 + 12 * (I - 1) * (I // 2) * I * 6)
+        alg_flops = 2.0 * B * (svd_mac + I * R1 * R1 + R1 * R1 * I * R1 + n_out * R1 + 2 * I * I * R1 * R1)
+
+        def step():
+            ttc.ttc_tt_svd_into(X, shape, c["eps"], TX.cores, rk_x, perm=px, stream=stream)
+            ttc.ttc_tt_svd_into(Y, shape, c["eps"], TY.cores, rk_y, perm=py, stream=stream)
+            ttc.ttc_contract(plan, TX, TY, out=zc, stream=stream)
+            ttc.ttc_reconstruct(ZD, plan.perm, out=out, stream=stream)
+        kernel_name = "alg2 pipeline (ttsvd x2, splice, reconstruct)"
     elif c["op"] == "reconstruct":
         n_el = c["I"] ** c["N"]
         out = torch.empty(B * n_el, dtype=torch.float32, device=dev)
@@ -268,7 +315,9 @@ def main():
             ttc.ttc_inner(XD, YD, out=out, stream=stream)
         kernel_name = "inner"
 
-    working_set = 4.0 * (X.cores.numel() + Y.cores.numel()) + 4.0 * out.numel()
+    xin = X.cores if hasattr(X, "cores") else X    # the step's device inputs (cores, or dense tensors for alg2)
+    yin = Y.cores if hasattr(Y, "cores") else Y
+    working_set = 4.0 * (xin.numel() + yin.numel()) + 4.0 * out.numel()
     flush = working_set < 2 * L2_BYTES
     flush_buf = torch.empty(int(2 * L2_BYTES // 4), dtype=torch.float32, device=dev) if flush else None
 
@@ -310,8 +359,8 @@ def main():
     # ---- e2e: the same metric through the public API from pinned host buffers (H2D + compute + D2H)
     e2e = None
     if not args.no_e2e:
-        hx = X.cores.to("cpu").pin_memory()
-        hy = Y.cores.to("cpu").pin_memory()
+        hx = xin.to("cpu").pin_memory()
+        hy = yin.to("cpu").pin_memory()
         hout = torch.empty(out.numel(), dtype=torch.float32).pin_memory()
         e_steps = max(3, min(args.steps, 10))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -319,8 +368,8 @@ def main():
             if it == 2:
                 torch.cuda.synchronize(dev)
                 e0.record(stream)
-            XD.cores.copy_(hx, non_blocking=True)
-            YD.cores.copy_(hy, non_blocking=True)
+            xin.copy_(hx, non_blocking=True)
+            yin.copy_(hy, non_blocking=True)
             step()
             hout.copy_(out, non_blocking=True)
         e1.record(stream)
@@ -362,8 +411,11 @@ def main():
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        Xh = ttgen.TTBatch(X.cores.cpu(), X.ranks, X.offsets, X.dims)
-        Yh = ttgen.TTBatch(Y.cores.cpu(), Y.ranks, Y.offsets, Y.dims)
+        if hasattr(X, "cores"):
+            Xh = ttgen.TTBatch(X.cores.cpu(), X.ranks, X.offsets, X.dims)
+            Yh = ttgen.TTBatch(Y.cores.cpu(), Y.ranks, Y.offsets, Y.dims)
+        else:
+            Xh, Yh = X.cpu(), Y.cpu()
         cb, _, _ = cpu_oracle_rate(cfg, Xh, Yh, args.cpu_seconds)
 
     if rank == 0:

@@ -302,6 +302,18 @@ def ttc_tt_svd_capacity(dims, perm=None) -> int:
     return cap.value
 
 
+def ttc_tt_svd_into(dense: torch.Tensor, dims, eps: float, cores: torch.Tensor, ranks: torch.Tensor, perm=None,
+                    stream=None) -> None:
+    """ttc_tt_svd into caller-owned device buffers (no host synchronisation): cores float32 [B * capacity],
+    ranks int32 [B, N + 1]."""
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
+    pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    n_el = int(np.prod(d.astype(np.int64)))
+    B = dense.numel() // max(n_el, 1)
+    _check(_lib.ttc_tt_svd(int(B), int(d.size), _ptr(d), _ptr(dense) if dense.numel() else None, _ptr(pm),
+                           float(eps), _ptr(cores), _ptr(ranks), _stream_handle(stream)))
+
+
 def ttc_tt_svd(dense: torch.Tensor, dims, eps: float, perm=None, stream=None) -> "TTDevice":
     """TT-SVD of B dense tensors (ttc.h: ttc_tt_svd; Alg. 1, optionally of the permuted X^rho of Alg. 2 step 1).
     dense: float32 [B * prod(dims)] on the device.  Returns the trains as a TTDevice (ranks read back to the host,

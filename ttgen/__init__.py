@@ -39,8 +39,12 @@ CONFIGS = {
     # TTCP output -- x_1^1 of two 20 x 20 x 20 tensors in TT format with ranks 20 is an order-4 train with
     # I = 20 and bonds 20 -- 160,000 floats per train
     "R1": dict(op="reconstruct", B=1024, N=4, I=20, R=20),
+    # the whole dense-input TTCP of Alg. 2 on Example 2 case (i): pairs of
+    # zero-mean unit-variance Gaussian 20 x 20 x 20 tensors, x_1^1, TT-SVD at eps = 0 (full ranks 20)
+    "A2": dict(op="alg2", B=1024, N=3, I=20, x_mode=1, y_mode=1, eps=0.0),
 }
-CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "S1": 6, "R1": 7}
+CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "S1": 6, "R1": 7, "A2": 8}
+
 DEFAULT_SEED = 20210901  # arXiv 2109.00626 submission month; recorded in every bench line
 SIDE_X, SIDE_Y = 0, 1
 
@@ -247,3 +251,19 @@ def config_batch(cfg: str, kind: str = "iid", b0: int = 0, B: Optional[int] = No
         return X, Y
     xr = uniform_ranks(B, c["N"], c["R"])
     return make_pair(kind, seed, cid, b0, xr, (c["I"],) * c["N"], None, rule="uniform", device=device)
+
+
+def dense_pairs(cfg: str, b0: int = 0, B: Optional[int] = None, seed: int = DEFAULT_SEED, device="cpu"):
+    """(X, Y) dense float32 [B * I^N] batches of an "alg2" workload: N(0, 1) values, seeded per pair and side
+    (Example 2: zero-mean, unit-variance Gaussian tensors)."""
+    c = CONFIGS[cfg]
+    B = c["B"] if B is None else B
+    n_el = c["I"] ** c["N"]
+    out = []
+    for side in (SIDE_X, SIDE_Y):
+        host = torch.empty(B * n_el, dtype=torch.float32)
+        for b in range(B):
+            g = torch.Generator().manual_seed(_seed(seed, CFG_ID[cfg], side, b0 + b))
+            host[b * n_el:(b + 1) * n_el] = torch.randn(n_el, generator=g, dtype=torch.float64).float()
+        out.append(host.to(device))
+    return tuple(out)
