@@ -18,7 +18,7 @@ namespace ttc {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSweeps = 12;   // cyclic Jacobi sweeps (quadratic convergence: n <= 64 needs < 10 in fp64)
+constexpr int kSweeps = 15;   // cap on cyclic Jacobi sweeps (quadratic convergence: n <= 64 needs < 10 in fp64)
 constexpr double kSigmaFloor = 1e-7;
 
 __device__ double block_sum(double v, double* red) {
@@ -36,10 +36,20 @@ __device__ double block_sum(double v, double* red) {
 // Symmetric eigenproblem of G (n x n, row-major in shared memory, overwritten by the rotated matrix) by cyclic
 // Jacobi; V (n x n) receives the eigenvectors as columns.  Round-robin ordering: n' = n rounded up to even
 // players, n'/2 disjoint rotations per round (player n' - 1 is a dummy when n is odd), n' - 1 rounds a sweep.
-__device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int* pp, int* pq) {
+__device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int* pp, int* pq, double* red) {
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) V[e] = (e / n == e % n) ? 1.0 : 0.0;
     const int np = (n + 1) & ~1, half = np / 2;
-    for (int sweep = 0; sweep < kSweeps; ++sweep)
+    for (int sweep = 0; sweep < kSweeps; ++sweep) {
+        // converged when the off-diagonal mass is below fp64 roundoff of the diagonal
+        __syncthreads();
+        double off = 0.0, dia = 0.0;
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+            const double v = G[e] * G[e];
+            if (e / n == e % n) dia += v; else off += v;
+        }
+        off = block_sum(off, red);
+        dia = block_sum(dia, red);
+        if (off <= 1e-30 * dia) break;
         for (int t = 0; t < np - 1; ++t) {
             __syncthreads();
             for (int q = threadIdx.x; q < half; q += blockDim.x) {
@@ -85,6 +95,7 @@ __device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int*
                 G[b * n + k] = s * gak + c * gbk;
             }
         }
+    }
     __syncthreads();
 }
 
@@ -136,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_kernel(const TtsvdArgs a) {
             G[i * side + j] = acc;
             G[j * side + i] = acc;
         }
-        jacobi(G, V, side, cs, sn, pp, pq);
+        jacobi(G, V, side, cs, sn, pp, pq, red);
         // ---- eigenvalues descending (stable order), the delta-truncated rank
         for (int j = threadIdx.x; j < side; j += blockDim.x) lam[j] = fmax(G[j * side + j], 0.0);
         __syncthreads();
