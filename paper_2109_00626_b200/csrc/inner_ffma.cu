@@ -141,28 +141,39 @@ __device__ __forceinline__ void block_fma(const float* __restrict__ A, int sA, c
     for (int a = 0; a < TA; ++a) Ap[a] = A + 8 * a * sA;
 #pragma unroll
     for (int b = 0; b < NB; ++b) Bp[b] = B + (c0 + lf + 4 * b) * sB;
+    // two k-chunks per iteration (K % 8 == 0): loads at immediate offsets +0 / +4 of pointers advanced once per
+    // iteration; the next iteration's first chunk is loaded while the second chunk computes (the final prefetch
+    // reads the 4 padding floats after every row / column: in bounds, discarded)
+    const float* ap[TA];
+    const float* bq[NB];
+#pragma unroll
+    for (int a = 0; a < TA; ++a) ap[a] = Ap[a];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) bq[b] = Bp[b];
     float4 za[TA], fb[NB];
 #pragma unroll
-    for (int a = 0; a < TA; ++a) za[a] = ld4(Ap[a]);
+    for (int a = 0; a < TA; ++a) za[a] = ld4(ap[a]);
 #pragma unroll
-    for (int b = 0; b < NB; ++b) fb[b] = ld4(Bp[b]);
-    // the iteration for the last chunk prefetches k = K: the 4 padding floats after every row / column (in
-    // bounds, discarded)
-#pragma unroll 2
-    for (int k = 4; k <= K; k += 4) {
-        float4 zn[TA], fn[NB];
+    for (int b = 0; b < NB; ++b) fb[b] = ld4(bq[b]);
+#pragma unroll 1
+    for (int k = 0; k < K; k += 8) {
+        float4 zb[TA], gb[NB];
 #pragma unroll
-        for (int a = 0; a < TA; ++a) zn[a] = ld4(Ap[a] + k);
+        for (int a = 0; a < TA; ++a) zb[a] = ld4(ap[a] + 4);
 #pragma unroll
-        for (int b = 0; b < NB; ++b) fn[b] = ld4(Bp[b] + k);
+        for (int b = 0; b < NB; ++b) gb[b] = ld4(bq[b] + 4);
 #pragma unroll
         for (int a = 0; a < TA; ++a)
 #pragma unroll
             for (int b = 0; b < NB; ++b) dot4x2(acc[a][b], za[a], fb[b]);
 #pragma unroll
-        for (int a = 0; a < TA; ++a) za[a] = zn[a];
+        for (int a = 0; a < TA; ++a) { ap[a] += 8; za[a] = ld4(ap[a]); }
 #pragma unroll
-        for (int b = 0; b < NB; ++b) fb[b] = fn[b];
+        for (int b = 0; b < NB; ++b) { bq[b] += 8; fb[b] = ld4(bq[b]); }
+#pragma unroll
+        for (int a = 0; a < TA; ++a)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) dot4x2(acc[a][b], zb[a], gb[b]);
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
