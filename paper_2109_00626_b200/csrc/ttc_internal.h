@@ -100,6 +100,8 @@ struct ReconArgs {
     int32_t  B, N, k;                   // split: left block = modes 1..k, right block = k+1..N (1 <= k < N)
     int32_t  rows, cols;                // prod_{n<=k} I_n, prod_{n>k} I_n
     int32_t  lbuf, t1, rbuf, t2;        // floats of: Left (+ same-parity partials), its temporary, Right, its temporary
+    int32_t  tm;                        // output tile 64 x 16 tm (tm = 4 or 5)
+    int32_t  ldl;                       // row stride of Left^T (rows rounded up to 64, + 4)
     int32_t  dims[TTC_MAX_ORDER];
     int64_t  ostride[TTC_MAX_ORDER];    // output stride of train mode n (permuted Eq. 2 order)
     TrainDev t;
