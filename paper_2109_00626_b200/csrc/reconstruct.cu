@@ -2,11 +2,17 @@
 // Alg. 2 steps 5-6: reconstruct, then permute).  One CTA per train:
 //   Left  = X_1 ... X_k          (prod_{n<=k} I_n  x  R_k), built left to right in shared memory
 //   Right = X_{k+1} ... X_N      (R_k  x  prod_{n>k} I_n), built right to left in shared memory
-//   D[row, col] = sum_r Left[row, r] Right[r, col]    (a register-tiled FP32 product)
+//   D[row, col] = sum_r Left[row, r] Right[r, col]
 // with row = (i_1..i_k) and col = (i_{k+1}..i_N) little-endian; the output address of (row, col) is
 // offr[row] + offc[col] (the permuted Eq. 2 strides), so the permutation of step 6 costs nothing extra.
-// Each core of a build step is first copied (coalesced) into shared memory, re-laid so that the threads of a
-// warp read it along odd strides (conflict-free), then the step's outputs are dot products over shared memory.
+//
+// Every product -- each build step and D itself -- is one register-tiled FP32 GEMM, out(m, n) = sum_q
+// At[q][m] B[n][q], with both operands in shared memory in layouts the Eq. 2 core layout gives for free:
+//   Left step  P_{j+1}^T[s][(pr, i)] = sum_r P_j^T[r][pr] X_j[(i, s)][r]     (X_j as stored: [i + I s][r])
+//   Right step Q_{j}[(i, pc)][r]     = sum_s X_j^T[s][(r, i)] Q_{j+1}[pc][s] (X_j as stored: [s][r + R i])
+//   D          D[row][col]           = sum_r Left^T[r][row] Right[col][r]
+// so each core is staged with a plain contiguous cp.async copy (no transposition), the partial products are
+// kept transposed / untransposed as the next GEMM reads them, and one tile routine serves all three.
 #include "ttc_internal.h"
 
 namespace ttc {
@@ -14,7 +20,7 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// Packed FP32 pair (FFMA2, sm_100a): acc.{x,y} accumulate the even / odd terms of a dot product.
+// Packed FP32 pair (FFMA2, sm_100a).
 __device__ __forceinline__ unsigned long long pk(float lo, float hi) {
     unsigned long long r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -23,116 +29,231 @@ __device__ __forceinline__ unsigned long long pk(float lo, float hi) {
 __device__ __forceinline__ void fma2(unsigned long long& acc, unsigned long long a, unsigned long long b) {
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
 }
-__device__ __forceinline__ float hsum2(unsigned long long v) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-    return lo + hi;
-}
-
-// D = Left Right in 64 x (16 TM) output tiles.  Thread (tx, ty) owns rows r0 + 4 tx + {0..3} (one 16-byte
-// load of Left^T per r: Left is kept transposed, Lt[r][row] with row stride ldL) and columns c0 + ty + 16 b,
-// b < TM (Right as Rt[col][r]: one 16-byte load per 4 r when Rk % 4 == 0).  Row pairs accumulate with FFMA2
-// (fma.rn.f32x2, the column value broadcast), so a thread's result for one column is a float4 of 4 consecutive
-// rows: one streaming 16-byte store when those rows are contiguous in the output (unpermuted leading modes).
 __device__ __forceinline__ float2 up(unsigned long long v) {
     float2 r;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
     return r;
 }
-template <int TM>
-__device__ __forceinline__ void d_tiles(const float* Lt, int ldL, const float* Rt, int Rk, int rows, int cols,
-                                        const int32_t* offr, const int32_t* offc, float* out) {
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const bool vec = (Rk & 3) == 0;
-    for (int r0 = 0; r0 < rows; r0 += 64)
-        for (int c0 = 0; c0 < cols; c0 += 16 * TM) {
-            const int row = r0 + 4 * tx;
-            const float* lt = Lt + row;
-            const float* rp[TM];
-#pragma unroll
-            for (int b2 = 0; b2 < TM; ++b2) rp[b2] = Rt + (size_t)min(c0 + ty + 16 * b2, cols - 1) * Rk;
-            unsigned long long acc[2][TM];
-#pragma unroll
-            for (int b2 = 0; b2 < TM; ++b2) acc[0][b2] = acc[1][b2] = 0ull;
-            if (vec) {
-                for (int r = 0; r < Rk; r += 4) {
-                    float4 lq[4], rv[TM];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) lq[q] = *reinterpret_cast<const float4*>(lt + (size_t)(r + q) * ldL);
-#pragma unroll
-                    for (int b2 = 0; b2 < TM; ++b2) rv[b2] = *reinterpret_cast<const float4*>(rp[b2] + r);
-#pragma unroll
-                    for (int b2 = 0; b2 < TM; ++b2) {
-                        const float w[4] = {rv[b2].x, rv[b2].y, rv[b2].z, rv[b2].w};
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            fma2(acc[0][b2], pk(lq[q].x, lq[q].y), pk(w[q], w[q]));
-                            fma2(acc[1][b2], pk(lq[q].z, lq[q].w), pk(w[q], w[q]));
-                        }
-                    }
-                }
-            } else {
-                for (int r = 0; r < Rk; ++r) {
-                    const float4 l = *reinterpret_cast<const float4*>(lt + (size_t)r * ldL);
-#pragma unroll
-                    for (int b2 = 0; b2 < TM; ++b2) {
-                        const float w = rp[b2][r];
-                        fma2(acc[0][b2], pk(l.x, l.y), pk(w, w));
-                        fma2(acc[1][b2], pk(l.z, l.w), pk(w, w));
-                    }
-                }
-            }
-            if (row >= rows) continue;
-            const int o0 = offr[row];
-            const bool v4 = row + 3 < rows && offr[row + 1] == o0 + 1 && offr[row + 2] == o0 + 2 && offr[row + 3] == o0 + 3;
-#pragma unroll
-            for (int b2 = 0; b2 < TM; ++b2) {
-                const int c = c0 + ty + 16 * b2;
-                if (c >= cols) continue;
-                float* oc = out + offc[c];
-                const float2 lo = up(acc[0][b2]), hi = up(acc[1][b2]);
-                if (v4 && (reinterpret_cast<uintptr_t>(oc + o0) & 15u) == 0) {
-                    __stcs(reinterpret_cast<float4*>(oc + o0), make_float4(lo.x, lo.y, hi.x, hi.y));
-                } else {
-                    const float v[4] = {lo.x, lo.y, hi.x, hi.y};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (row + u < rows) __stcs(oc + offr[row + u], v[u]);
-                }
-            }
-        }
-}
-
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float lds1(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Left[row][r] (row stride Rk), Right stored transposed Rt[col][r] (col stride Rk): both contiguous along r.
+// Contiguous copy of n floats global -> shared (16-byte pieces when both ends are aligned).
+__device__ __forceinline__ void stage(float* dst, const float* src, int n) {
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u) == 0) {
+        for (int e = threadIdx.x; e < (n >> 2); e += blockDim.x) cp_async16(dst + 4 * e, src + 4 * e);
+        for (int e = (n & ~3) + threadIdx.x; e < n; e += blockDim.x) cp_async4(dst + e, src + e);
+    } else {
+        for (int e = threadIdx.x; e < n; e += blockDim.x) cp_async4(dst + e, src + e);
+    }
+}
+
+// Thread grid of one GEMM: txn = lx wx threads along m (4 rows each), tyn = (32 / lx) (8 / wx) along n (tm
+// columns each, 4 or 5); a warp covers lx x (32 / lx) of it, so its At loads touch lx distinct 16-byte quads and
+// its B loads 32 / lx distinct columns.  Chosen per product shape by a cost model: tiles x max(FFMA2 time,
+// shared-memory wavefronts) per k, FFMA2 ~ tm and wavefronts ~ max(1, lx / 8) + tm / 4 max(1, ly / 8).
+struct Grid {
+    int lx, wx, tm;
+};
+// The 40 candidates (lx, wx, tm) are scored by the first 40 threads in parallel; *best (shared, initialised to
+// ~0 by the caller before a barrier) receives the winner packed as cost << 8 | candidate.
+__device__ __forceinline__ Grid grid_of(int c) { return Grid{1 << (c >> 3), 1 << ((c >> 1) & 3), 4 + (c & 1)}; }
+__device__ __forceinline__ void score_grid(int M, int N, unsigned* best) {
+    const int c = threadIdx.x;
+    if (c >= 40) return;
+    const Grid g = grid_of(c);
+    const int ly = 32 / g.lx, txn = g.lx * g.wx, tyn = ly * (8 / g.wx), tm = g.tm;
+    const int tiles = ((M + 4 * txn - 1) / (4 * txn)) * ((N + tyn * tm - 1) / (tyn * tm));
+    // per-k cost in quarter units: FFMA2 4 tm; wavefronts 4 max(1, lx/8) + tm max(1, ly/8)
+    const int wf = 4 * max(1, g.lx / 8) + tm * max(1, ly / 8);
+    atomicMin(best, ((unsigned)min(tiles * max(4 * tm, wf), 0xffffff) << 8) | (unsigned)c);
+}
+
+// out(m, n) = sum_{q < K} At[q lda + m] B[n ldb + q] for m < M, n < N.  Thread (tx, ty) of the grid owns
+// m0 + {0..3} (m0 = mt + 4 tx, one 16-byte At load per q when lda % 4 == 0; At must be readable up to row
+// m = 4 txn ceil(M / (4 txn)) - 1 < M + 512) and n = nt + ty + tyn b, b < TM (one 16-byte B load per 4 q when ldb, K % 4
+// == 0; columns past N re-read column N - 1).  The m pairs accumulate with FFMA2 (the B value broadcast);
+// st.row(m0) once per tile, then st(row state, n, v) stores the thread's 4 results of column n.
+template <int TM, class Store>
+__device__ __forceinline__ void tile_gemm(const Grid g, const float* At, int lda, const float* B, int ldb, int M,
+                                          int N, int K, const Store& st) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, ly = 32 / g.lx;
+    const int txn = g.lx * g.wx, tyn = ly * (8 / g.wx);
+    const int tx = (warp % g.wx) * g.lx + (lane & (g.lx - 1)), ty = (warp / g.wx) * ly + lane / g.lx;
+    const bool vecA = (lda & 3) == 0, vecB = ((ldb | K) & 3) == 0;
+    const uint32_t A0 = sa(At), B0 = sa(B);
+    const int la = 4 * lda;   // bytes per q row of At
+    for (int mt = 0; mt < M; mt += 4 * txn)
+        for (int nt = 0; nt < N; nt += tyn * TM) {
+            const int m0 = mt + 4 * tx;
+            uint32_t ap = A0 + 4u * m0;
+            uint32_t bp[TM];
+#pragma unroll
+            for (int b2 = 0; b2 < TM; ++b2) bp[b2] = B0 + 4u * (uint32_t)(min(nt + ty + tyn * b2, N - 1) * ldb);
+            unsigned long long acc[2][TM];
+#pragma unroll
+            for (int b2 = 0; b2 < TM; ++b2) acc[0][b2] = acc[1][b2] = 0ull;
+            if (vecA && vecB) {
+                for (int q = 0; q < K; q += 4, ap += 4 * la) {
+                    float4 a4[4], b4[TM];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) a4[u] = lds4(ap + u * la);
+#pragma unroll
+                    for (int b2 = 0; b2 < TM; ++b2) b4[b2] = lds4(bp[b2] + 4 * q);
+#pragma unroll
+                    for (int b2 = 0; b2 < TM; ++b2) {
+                        const float w[4] = {b4[b2].x, b4[b2].y, b4[b2].z, b4[b2].w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            fma2(acc[0][b2], pk(a4[u].x, a4[u].y), pk(w[u], w[u]));
+                            fma2(acc[1][b2], pk(a4[u].z, a4[u].w), pk(w[u], w[u]));
+                        }
+                    }
+                }
+            } else {
+                for (int q = 0; q < K; ++q, ap += la) {
+                    float4 a;
+                    if (vecA) a = lds4(ap);
+                    else a = make_float4(lds1(ap), lds1(ap + 4), lds1(ap + 8), lds1(ap + 12));
+#pragma unroll
+                    for (int b2 = 0; b2 < TM; ++b2) {
+                        const float w = lds1(bp[b2] + 4 * q);
+                        fma2(acc[0][b2], pk(a.x, a.y), pk(w, w));
+                        fma2(acc[1][b2], pk(a.z, a.w), pk(w, w));
+                    }
+                }
+            }
+            if (m0 >= M) continue;
+            const auto rs = st.row(m0);
+#pragma unroll
+            for (int b2 = 0; b2 < TM; ++b2) {
+                const int n = nt + ty + tyn * b2;
+                if (n >= N) continue;
+                const float2 lo = up(acc[0][b2]), hi = up(acc[1][b2]);
+                st(rs, n, make_float4(lo.x, lo.y, hi.x, hi.y));
+            }
+        }
+}
+template <class Store>
+__device__ __forceinline__ void gemm(const Grid g, const float* At, int lda, const float* B, int ldb, int M, int N,
+                                     int K, const Store& st) {
+    if (g.tm == 5) tile_gemm<5>(g, At, lda, B, ldb, M, N, K, st);
+    else tile_gemm<4>(g, At, lda, B, ldb, M, N, K, st);
+}
+
+// Stores of the three GEMM kinds (row state from row(m0), computed once per tile).  Rows m0 + u >= M dropped.
+struct RowSt {
+    int m0, a, b;
+};
+struct StoreLeft {   // P'^T[s][pr + prow i] (row stride ld), m = pr, n = i + I s
+    float* out;
+    int ld, prow, I, M;
+    __device__ __forceinline__ RowSt row(int m0) const { return RowSt{m0, m0 + 3 < M ? 4 : M - m0, 0}; }
+    __device__ __forceinline__ void operator()(const RowSt& rs, int n, float4 v) const {
+        const int s = n / I, i = n - s * I;
+        float* o = out + (size_t)s * ld + prow * i + rs.m0;
+        if (rs.a == 4 && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+            *reinterpret_cast<float4*>(o) = v;
+        } else {
+            const float w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u < rs.a) o[u] = w[u];
+        }
+    }
+};
+struct StoreRight {  // Q'[i + I pc][r] (row stride R), m = r + R i, n = pc
+    float* out;
+    int R, I, M;
+    __device__ __forceinline__ RowSt row(int m0) const {
+        const int i0 = m0 / R;
+        return RowSt{m0, i0, m0 - i0 * R};
+    }
+    __device__ __forceinline__ void operator()(const RowSt& rs, int n, float4 v) const {
+        const float w[4] = {v.x, v.y, v.z, v.w};
+        if (rs.b + 3 < R) {   // the 4 rows lie in one row of Q' (M = R I, so m0 + 3 < M as well)
+            float* o = out + ((size_t)rs.a + (size_t)I * n) * R + rs.b;
+            if ((reinterpret_cast<uintptr_t>(o) & 15u) == 0) { *reinterpret_cast<float4*>(o) = v; return; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[u] = w[u];
+            return;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int m = rs.m0 + u;
+            if (m >= M) break;
+            const int i = m / R, r = m - i * R;
+            out[((size_t)i + (size_t)I * n) * R + r] = w[u];
+        }
+    }
+};
+struct StoreD {      // out[offr[row] + offc[col]], m = row, n = col (streaming 16-byte stores when contiguous)
+    float* out;
+    const int32_t* offr;
+    const int32_t* offc;
+    int M;
+    __device__ __forceinline__ RowSt row(int m0) const {
+        const int o0 = offr[m0];
+        const bool v4 = m0 + 3 < M && offr[m0 + 1] == o0 + 1 && offr[m0 + 2] == o0 + 2 && offr[m0 + 3] == o0 + 3;
+        return RowSt{m0, o0, v4 ? 1 : 0};
+    }
+    __device__ __forceinline__ void operator()(const RowSt& rs, int n, float4 v) const {
+        float* o = out + offc[n] + rs.a;
+        if (rs.b && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+            __stcs(reinterpret_cast<float4*>(o), v);
+            return;
+        }
+        const float w[4] = {v.x, v.y, v.z, v.w};
+        float* oc = out + offc[n];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (rs.m0 + u < M) __stcs(oc + offr[rs.m0 + u], w[u]);
+    }
+};
+
 __global__ void __launch_bounds__(kThreads, 2) reconstruct_kernel(const ReconArgs a) {
     extern __shared__ float sm[];
     __shared__ int32_t rk[TTC_MAX_ORDER + 1];
     __shared__ int64_t co[TTC_MAX_ORDER + 1];
+    __shared__ unsigned gsel[2];                // packed grid choices (score_grid), alternating between GEMMs
     const int b = blockIdx.x, N = a.N, k = a.k;
     for (int n = threadIdx.x; n <= N; n += blockDim.x)
         rk[n] = (n == 0 || n == N) ? 1 : (a.t.ranks ? a.t.ranks[(int64_t)b * (N + 1) + n] : a.t.urank);
     __syncthreads();
+    const int rows = a.rows, cols = a.cols;
+    int gi = 0;                                 // gsel slot of the next GEMM
     if (threadIdx.x == 0) {
+        gsel[0] = gsel[1] = ~0u;
         co[0] = 0;
         for (int n = 0; n < N; ++n) co[n + 1] = co[n] + (int64_t)rk[n] * a.dims[n] * rk[n + 1];
     }
-    __syncthreads();
     const float* G = a.t.cores + (a.t.offsets ? a.t.offsets[b] : (int64_t)b * a.t.train_elems);
     float* out = a.out + (a.out_offsets ? a.out_offsets[b] : (int64_t)b * a.pair_elems);
-    const int Rk = rk[k];
-    const int rows = a.rows, cols = a.cols;
-    float* L = sm;                                  // Left^T: Rk x rows (row stride ldL); partials [row][s]
-    float* Rt = L + a.lbuf;                         // cols x Rk (col stride Rk)
-    float* T = Rt + a.rbuf;                         // Left's build temporary
-    float* T2 = T + a.t1;                           // Right's build temporary
+    float* L = sm;                          // Left^T: Rk x rows, row stride ldl; left partials likewise
+    float* Rt = L + a.lbuf;                 // Right: [col][r], row stride Rk; right partials likewise
+    float* T = Rt + a.rbuf;                 // Left's build temporary
+    float* T2 = T + a.t1;                   // Right's build temporary
     int32_t* offr = reinterpret_cast<int32_t*>(T2 + a.t2);
     int32_t* offc = offr + rows;
+    float* XS = reinterpret_cast<float*>(offc + cols);   // the staged core of the current build step
+    XS = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(XS) + 15) & ~uintptr_t(15));
     // output offsets of the row / column multi-indices (permuted Eq. 2 strides)
     for (int r = threadIdx.x; r < rows; r += blockDim.x) {
         int64_t o = 0;
@@ -146,110 +267,64 @@ __global__ void __launch_bounds__(kThreads, 2) reconstruct_kernel(const ReconArg
         for (int n = k; n < N; ++n) { const int i = q % a.dims[n]; q /= a.dims[n]; o += (int64_t)i * a.ostride[n]; }
         offc[c] = (int32_t)o;
     }
-    float* XS = reinterpret_cast<float*>(offc + cols);   // the staged core of the current build step
-    // ---- Left = X_1 .. X_k: P[row][s], row = (i_1..i_j) little-endian; the last product lands in L,
-    // transposed (Lt[s][row], row stride ldL)
-    const int ldL = a.ldl;
+    __syncthreads();
+    const int Rk = rk[k];
+    // ---- Left: P_1^T[s][i] = X_1[0, i, s] (as stored), then P_{j+1}^T = GEMM(P_j^T, X_j) for j = 2..k
     {
-        float* cur = (k % 2 == 1) ? L : T;          // k - 1 products follow: alternate so the last writes L
-        int prow = a.dims[0];
-        const float* X1 = G + co[0];                // X_1[0, i, s] at i + I_1 s
-        if (k == 1) {
-            for (int e = threadIdx.x; e < prow * rk[1]; e += blockDim.x) {
-                const int s = e / prow, i = e - s * prow;
-                cur[s * ldL + i] = __ldg(X1 + e);
-            }
-        } else {
-            for (int e = threadIdx.x; e < prow * rk[1]; e += blockDim.x) {
-                const int i = e / rk[1], s = e - i * rk[1];
-                cur[e] = __ldg(X1 + i + a.dims[0] * s);
-            }
+        float* cur = (k % 2 == 1) ? L : T;  // k - 1 products follow: alternate so the last writes L
+        int prow = a.dims[0], ld = a.ld[0];
+        const float* X1 = G + co[0];
+        for (int e = threadIdx.x; e < prow * rk[1]; e += blockDim.x) {
+            const int s = e / prow, i = e - s * prow;
+            cur[s * ld + i] = __ldg(X1 + e);
         }
         for (int j = 1; j < k; ++j) {
-            const float* Xj = G + co[j];            // X_j[r, i, s] at r + R (i + I s)
-            const int R = rk[j], S = rk[j + 1], I = a.dims[j], Rp = R | 1;
-            __syncthreads();                        // cur written, XS free
-            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-            for (int s = 0; s < S; ++s)             // XS[(i S + s) Rp + r] = X_j[r, i, s]
-                for (int i = warp; i < I; i += nw)
-                    for (int r = lane; r < R; r += 32) cp_async4(XS + (i * S + s) * Rp + r, Xj + r + R * (i + I * s));
+            const int R = rk[j], S = rk[j + 1], I = a.dims[j];
+            stage(XS, G + co[j], R * I * S);   // [i + I s][r]
+            score_grid(prow, I * S, &gsel[gi]);
             cp_wait_all();
-            __syncthreads();
+            __syncthreads();                   // cur and XS ready
             float* nxt = (cur == L) ? T : L;
-            const bool last = j == k - 1;           // writes Left^T
-            const int nrow = prow * I, ig = (I + 3) >> 2;
-            // thread: (pr, i0..i0+3, s), s fastest across threads (XS rows Rp apart: odd stride, no conflicts)
-            for (int e = threadIdx.x; e < prow * ig * S; e += blockDim.x) {
-                const int s = e % S, t = e / S, gi = t % ig, pr = t / ig, i0 = 4 * gi;
-                const float* p = cur + (size_t)pr * R;
-                const float* x[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) x[u] = XS + (min(i0 + u, I - 1) * S + s) * Rp;
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-                for (int r = 0; r < R; ++r) {
-                    const float pv = p[r];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) acc[u] = fmaf(pv, x[u][r], acc[u]);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (i0 + u < I) {
-                        const int row = pr + prow * (i0 + u);
-                        nxt[last ? s * ldL + row : row * S + s] = acc[u];
-                    }
-            }
+            const int nld = a.ld[j];
+            const Grid g = grid_of(gsel[gi] & 255u);
+            if (threadIdx.x == 0) gsel[gi ^ 1] = ~0u;   // the slot after next is reset behind the next barrier
+            gi ^= 1;
+            gemm(g, cur, ld, XS, R, prow, I * S, R, StoreLeft{nxt, nld, prow, I, prow});
+            __syncthreads();                   // XS free, nxt complete
             cur = nxt;
-            prow = nrow;
+            prow *= I;
+            ld = nld;
         }
     }
-    // ---- Right = X_{k+1} .. X_N: Q[col][r], col = (i_j..i_N) little-endian; the last product lands in Rt
-    if (k == N) {                                   // N = 1: no right block, Right = [1]
+    // ---- Right: Q_N[i][r] = X_N[r, i, 0] (as stored), then Q_j = GEMM(X_j^T, Q_{j+1}) for j = N-1..k+1
+    if (k == N) {                           // N = 1: no right block, Right = [1]
         if (threadIdx.x == 0) Rt[0] = 1.f;
     } else {
-        const int nR = N - k;                       // cores in the right block
+        const int nR = N - k;
         float* cur = (nR % 2 == 1) ? Rt : T2;
         int pcol = a.dims[N - 1];
-        const float* XN = G + co[N - 1];            // X_N[r, i, 0] at r + R i
-        const int RN = rk[N - 1];
-        for (int e = threadIdx.x; e < pcol * RN; e += blockDim.x) cur[e] = __ldg(XN + e);   // [i][r] = X_N[r, i]
+        const float* XN = G + co[N - 1];
+        for (int e = threadIdx.x; e < pcol * rk[N - 1]; e += blockDim.x) cur[e] = __ldg(XN + e);
         for (int j = N - 2; j >= k; --j) {
-            const float* Xj = G + co[j];
-            const int R = rk[j], S = rk[j + 1], I = a.dims[j], Sp = S | 1;
-            __syncthreads();
-            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-            for (int s = warp; s < S; s += nw)      // XS[(r + R i) Sp + s] = X_j[r, i, s]
-                for (int ri = lane; ri < R * I; ri += 32) cp_async4(XS + ri * Sp + s, Xj + ri + R * I * s);
+            const int R = rk[j], S = rk[j + 1], I = a.dims[j];
+            stage(XS, G + co[j], R * I * S);   // [s][r + R i]
+            score_grid(R * I, pcol, &gsel[gi]);
             cp_wait_all();
             __syncthreads();
             float* nxt = (cur == Rt) ? T2 : Rt;
-            const int ncol = I * pcol, ig = (I + 3) >> 2;
-            // thread: (r, i0..i0+3, pc), r fastest across threads (XS rows Sp apart: odd stride, no conflicts)
-            for (int e = threadIdx.x; e < pcol * ig * R; e += blockDim.x) {
-                const int r = e % R, t = e / R, gi = t % ig, pc = t / ig, i0 = 4 * gi;
-                const float* q = cur + (size_t)pc * S;
-                const float* x[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) x[u] = XS + (r + R * min(i0 + u, I - 1)) * Sp;
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-                for (int s2 = 0; s2 < S; ++s2) {
-                    const float qv = q[s2];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) acc[u] = fmaf(x[u][s2], qv, acc[u]);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (i0 + u < I) nxt[(i0 + u + I * pc) * R + r] = acc[u];
-            }
+            const Grid g = grid_of(gsel[gi] & 255u);
+            if (threadIdx.x == 0) gsel[gi ^ 1] = ~0u;
+            gi ^= 1;
+            gemm(g, XS, R * I, cur, S, R * I, pcol, S, StoreRight{nxt, R, I, R * I});
+            __syncthreads();
             cur = nxt;
-            pcol = ncol;
+            pcol *= I;
         }
     }
+    score_grid(rows, cols, &gsel[gi]);
     __syncthreads();
-    // ---- D = Left Right in 64 x (16 TM) output tiles (TM = 5 when 80-wide tiles waste less of the ragged edge)
-    if (a.tm == 5) d_tiles<5>(L, ldL, Rt, Rk, rows, cols, offr, offc, out);
-    else d_tiles<4>(L, ldL, Rt, Rk, rows, cols, offr, offc, out);
+    // ---- D = Left Right, written through the permuted output offsets
+    gemm(grid_of(gsel[gi] & 255u), L, a.ldl, Rt, Rk, rows, cols, Rk, StoreD{out, offr, offc, rows});
 }
 
 }  // namespace

@@ -283,26 +283,26 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
     std::vector<int64_t> pre(N + 1, 1), suf(N + 1, 1);
     for (int n = 0; n < N; ++n) pre[n + 1] = pre[n] * t->dims[n];
     for (int n = N - 1; n >= 0; --n) suf[n] = suf[n + 1] * t->dims[n];
-    auto ldl = [](int64_t rows) { return ((rows + 63) & ~int64_t(63)) + 4; };
+    auto ldl = [](int64_t rows) { return (rows + 3) & ~int64_t(3); };   // 16-byte rows (tile over-reads of the
+                                                                         // last row land in the next buffer)
     for (int k = 1; k <= (N == 1 ? 1 : N - 1); ++k) {
         // the left chain's partial products P_j (pre[j] x R_j, j = 1..k) alternate between Left and its
         // temporary so that P_k lands in Left; the right chain's Q_j (R_j x suf[j], j = N-1..k) likewise
-        // plus the staged core of a build step (cores 2..k and k+1..N-1, rows padded to an odd length)
+        // plus the staged core of a build step (cores 2..N-1 as stored)
         int64_t lb = 0, t1 = 0, rb = N == 1 ? 1 : 0, t2 = 0, xs = 0;
         for (int b = 0; b < B; ++b) {
-            for (int j = 1; j <= k; ++j) {   // P_k is stored transposed with row stride ldl(k)
-                const int64_t v = (j == k ? ldl(pre[k]) : pre[j]) * h.rank(b, j);
+            for (int j = 1; j <= k; ++j) {   // P_j^T: R_j rows of ldl(pre[j]) floats
+                const int64_t v = ldl(pre[j]) * h.rank(b, j);
                 if ((k - j) % 2 == 0) lb = std::max(lb, v); else t1 = std::max(t1, v);
             }
             for (int j = k; j < N; ++j) {
                 const int64_t v = suf[j] * h.rank(b, j);
                 if ((j - k) % 2 == 0) rb = std::max(rb, v); else t2 = std::max(t2, v);
             }
-            for (int j = 1; j < k; ++j)
-                xs = std::max(xs, (int64_t)t->dims[j] * h.rank(b, j + 1) * (h.rank(b, j) | 1));
-            for (int j = k; j < N - 1; ++j)
-                xs = std::max(xs, (int64_t)t->dims[j] * h.rank(b, j) * (h.rank(b, j + 1) | 1));
+            for (int j = 1; j < N - 1; ++j)
+                xs = std::max(xs, (int64_t)t->dims[j] * h.rank(b, j) * h.rank(b, j + 1));
         }
+        xs += 512 + 4;   // tile over-reads past the last buffer (4 rows x 128 threads) + 16-byte alignment
         auto r4 = [](int64_t v) { return (v + 3) & ~int64_t(3); };   // keep every buffer 16-byte aligned
         lb = r4(lb); t1 = r4(t1); rb = r4(rb); t2 = r4(t2);
         const int64_t bytes = 4 * (lb + t1 + rb + t2 + pre[k] + suf[k] + xs);
@@ -319,6 +319,7 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
     a.cols = (int32_t)suf[best_k];
     a.lbuf = (int32_t)bl; a.t1 = (int32_t)bt1; a.rbuf = (int32_t)br; a.t2 = (int32_t)bt2;
     a.ldl = (int32_t)ldl(a.rows);
+    for (int j = 0; j < best_k; ++j) a.ld[j] = (int32_t)ldl(pre[j + 1]);
     a.tm = (a.cols + 79) / 80 * 80 < (a.cols + 63) / 64 * 64 ? 5 : 4;   // 80 columns when that pads less
     for (int n = 0; n < N; ++n) { a.dims[n] = t->dims[n]; a.ostride[n] = ostride[n]; }
     a.t = to_dev(h);

@@ -101,7 +101,8 @@ struct ReconArgs {
     int32_t  rows, cols;                // prod_{n<=k} I_n, prod_{n>k} I_n
     int32_t  lbuf, t1, rbuf, t2;        // floats of: Left (+ same-parity partials), its temporary, Right, its temporary
     int32_t  tm;                        // output tile 64 x 16 tm (tm = 4 or 5)
-    int32_t  ldl;                       // row stride of Left^T (rows rounded up to 64, + 4)
+    int32_t  ldl;                       // row stride of Left^T (rows rounded up to a multiple of 4)
+    int32_t  ld[TTC_MAX_ORDER];         // row stride of the left partial P_{j+1}^T (= ldl for j = k - 1)
     int32_t  dims[TTC_MAX_ORDER];
     int64_t  ostride[TTC_MAX_ORDER];    // output stride of train mode n (permuted Eq. 2 order)
     TrainDev t;
