@@ -836,7 +836,22 @@ ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const
         sa.out = out_cores_dev;
         sa.out_offsets = out_offsets_dev;
         sa.out_pair_elems = p->B ? p->total / p->B : 0;
-        e = ttc::launch_splice(sa, sizeof(float) * (size_t)p->k_floats, s);
+        // whole trains staged in shared memory (one round trip for all of a pair's loads) when they fit
+        auto max_elems = [](const HostTrain& h) {
+            if (h.uniform) return h.train_elems_uniform;
+            int64_t m = 0;
+            for (const int64_t v : h.sizes) m = std::max(m, v);
+            return m;
+        };
+        const int64_t sx = (max_elems(hx) + 3) & ~int64_t(3), sy = (max_elems(hy) + 3) & ~int64_t(3);
+        sa.k4 = (int32_t)((p->k_floats + 3) & ~int64_t(3));
+        size_t smem = sizeof(float) * (size_t)sa.k4;
+        if (4 * (sx + sy) + smem <= 48 * 1024) {
+            sa.stage_x = (int32_t)sx;
+            sa.stage_y = (int32_t)sy;
+            smem += 4 * (size_t)(sx + sy);
+        }
+        e = ttc::launch_splice(sa, smem, s);
         if (e != cudaSuccess) return cuda_fail(e, "ttc_contract (splice) launch");
         return TTC_OK;
     }

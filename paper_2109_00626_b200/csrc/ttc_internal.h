@@ -92,6 +92,8 @@ struct SpliceArgs {
     float*   out;
     const int64_t* out_offsets;         // device [B] or nullptr (uniform)
     int64_t  out_pair_elems;
+    int32_t  k4;                        // floats of SMEM for K (rounded up to 4)
+    int32_t  stage_x, stage_y;          // floats of SMEM for the whole X / Y train (0: cores read from global)
 };
 cudaError_t launch_splice(const SpliceArgs& a, size_t smem_bytes, cudaStream_t s);
 
