@@ -36,20 +36,14 @@ __device__ double block_sum(double v, double* red) {
 // Symmetric eigenproblem of G (n x n, row-major in shared memory, overwritten by the rotated matrix) by cyclic
 // Jacobi; V (n x n) receives the eigenvectors as columns.  Round-robin ordering: n' = n rounded up to even
 // players, n'/2 disjoint rotations per round (player n' - 1 is a dummy when n is odd), n' - 1 rounds a sweep.
-__device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int* pp, int* pq, double* red) {
+// A pair is rotated only while |g_pq| > eps_64 sqrt(|g_pp g_qq|) (below that the rotation changes nothing at
+// fp64 precision); the iteration stops after a sweep that rotated no pair (or kSweeps sweeps).
+__device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int* pp, int* pq, int* flag) {
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) V[e] = (e / n == e % n) ? 1.0 : 0.0;
     const int np = (n + 1) & ~1, half = np / 2;
     for (int sweep = 0; sweep < kSweeps; ++sweep) {
-        // converged when the off-diagonal mass is below fp64 roundoff of the diagonal
         __syncthreads();
-        double off = 0.0, dia = 0.0;
-        for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-            const double v = G[e] * G[e];
-            if (e / n == e % n) dia += v; else off += v;
-        }
-        off = block_sum(off, red);
-        dia = block_sum(dia, red);
-        if (off <= 1e-30 * dia) break;
+        if (threadIdx.x == 0) *flag = 0;
         for (int t = 0; t < np - 1; ++t) {
             __syncthreads();
             for (int q = threadIdx.x; q < half; q += blockDim.x) {
@@ -58,23 +52,27 @@ __device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int*
                 int a = pos(q), b = pos(np - 1 - q);
                 if (a > b) { const int x = a; a = b; b = x; }
                 double c = 1.0, s = 0.0;
+                bool rot = false;
                 if (b < n) {
                     const double app = G[a * n + a], aqq = G[b * n + b], apq = G[a * n + b];
-                    if (fabs(apq) > 1e-300 && fabs(apq) > DBL_EPSILON * 1e-3 * sqrt(fabs(app * aqq))) {
+                    if (fabs(apq) > 1e-300 && fabs(apq) > DBL_EPSILON * sqrt(fabs(app * aqq))) {
                         const double th = (aqq - app) / (2.0 * apq);
                         const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
                         c = 1.0 / sqrt(tt * tt + 1.0);
                         s = tt * c;
+                        rot = true;
                     }
                 }
-                cs[q] = c; sn[q] = s; pp[q] = a; pq[q] = b < n ? b : -1;
+                if (rot) *flag = 1;
+                cs[q] = c; sn[q] = s; pp[q] = a; pq[q] = rot ? b : -1;
             }
             __syncthreads();
             // columns p, q of G and V
             for (int e = threadIdx.x; e < half * n; e += blockDim.x) {
                 const int q = e / n, k = e - q * n;
-                if (pq[q] < 0 || sn[q] == 0.0) continue;
-                const int a = pp[q], b = pq[q];
+                const int b = pq[q];
+                if (b < 0) continue;
+                const int a = pp[q];
                 const double c = cs[q], s = sn[q];
                 const double gka = G[k * n + a], gkb = G[k * n + b];
                 G[k * n + a] = c * gka - s * gkb;
@@ -87,14 +85,17 @@ __device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int*
             // rows p, q of G
             for (int e = threadIdx.x; e < half * n; e += blockDim.x) {
                 const int q = e / n, k = e - q * n;
-                if (pq[q] < 0 || sn[q] == 0.0) continue;
-                const int a = pp[q], b = pq[q];
+                const int b = pq[q];
+                if (b < 0) continue;
+                const int a = pp[q];
                 const double c = cs[q], s = sn[q];
                 const double gak = G[a * n + k], gbk = G[b * n + k];
                 G[a * n + k] = c * gak - s * gbk;
                 G[b * n + k] = s * gak + c * gbk;
             }
         }
+        __syncthreads();
+        if (*flag == 0) break;
     }
     __syncthreads();
 }
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_kernel(const TtsvdArgs a) {
     int* order = reinterpret_cast<int*>(red + 32);               // gmax
     int* pp = order + side_max;
     int* pq = pp + side_max / 2 + 1;
-    int* misc = pq + side_max / 2 + 1;                           // [0]: R
+    int* misc = pq + side_max / 2 + 1;                           // [0]: R, [1]: Jacobi rotation flag
     float* Z = reinterpret_cast<float*>(misc + 4) + ((4 - ((reinterpret_cast<uintptr_t>(misc + 4) >> 2) & 3)) & 3);
     float* Zt = Z + a.elems;
     const float* src = a.dense + (int64_t)b * a.elems;
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_kernel(const TtsvdArgs a) {
             G[i * side + j] = acc;
             G[j * side + i] = acc;
         }
-        jacobi(G, V, side, cs, sn, pp, pq, red);
+        jacobi(G, V, side, cs, sn, pp, pq, misc + 1);
         // ---- eigenvalues descending (stable order), the delta-truncated rank
         for (int j = threadIdx.x; j < side; j += blockDim.x) lam[j] = fmax(G[j * side + j], 0.0);
         __syncthreads();
