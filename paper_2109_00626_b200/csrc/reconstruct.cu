@@ -3,7 +3,8 @@
 //   Left  = X_1 ... X_k          (prod_{n<=k} I_n  x  R_k), built left to right in shared memory
 //   Right = X_{k+1} ... X_N      (R_k  x  prod_{n>k} I_n), built right to left in shared memory
 //   D[row, col] = sum_r Left[row, r] Right[r, col]
-// with row = (i_1..i_k) and col = (i_{k+1}..i_N) little-endian; the output address of (row, col) is
+// with row = (i_1..i_k) (little-endian, or big-endian when that puts the output's stride-1 mode first) and
+// col = (i_{k+1}..i_N) little-endian; the output address of (row, col) is
 // offr[row] + offc[col] (the permuted Eq. 2 strides), so the permutation of step 6 costs nothing extra.
 //
 // Every product -- each build step and D itself -- is one register-tiled FP32 GEMM, out(m, n) = sum_q
@@ -162,12 +163,21 @@ __device__ __forceinline__ void gemm(const Grid g, const float* At, int lda, con
 struct RowSt {
     int m0, a, b;
 };
-struct StoreLeft {   // P'^T[s][pr + prow i] (row stride ld), m = pr, n = i + I s
+struct StoreLeft {   // P'^T[s][row] (row stride ld), m = pr, n = i + I s; row = pr + prow i, or i + I pr (rev)
     float* out;
     int ld, prow, I, M;
+    bool rev;
     __device__ __forceinline__ RowSt row(int m0) const { return RowSt{m0, m0 + 3 < M ? 4 : M - m0, 0}; }
     __device__ __forceinline__ void operator()(const RowSt& rs, int n, float4 v) const {
         const int s = n / I, i = n - s * I;
+        if (rev) {   // the new mode fastest: the 4 rows are I apart
+            float* o = out + (size_t)s * ld + i + I * rs.m0;
+            const float w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u < rs.a) o[I * u] = w[u];
+            return;
+        }
         float* o = out + (size_t)s * ld + prow * i + rs.m0;
         if (rs.a == 4 && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
             *reinterpret_cast<float4*>(o) = v;
@@ -258,7 +268,11 @@ __global__ void __launch_bounds__(kThreads, 2) reconstruct_kernel(const ReconArg
     for (int r = threadIdx.x; r < rows; r += blockDim.x) {
         int64_t o = 0;
         int q = r;
-        for (int n = 0; n < k; ++n) { const int i = q % a.dims[n]; q /= a.dims[n]; o += (int64_t)i * a.ostride[n]; }
+        if (a.lrev) {   // rows enumerate the left modes big-endian (mode k fastest)
+            for (int n = k - 1; n >= 0; --n) { const int i = q % a.dims[n]; q /= a.dims[n]; o += (int64_t)i * a.ostride[n]; }
+        } else {
+            for (int n = 0; n < k; ++n) { const int i = q % a.dims[n]; q /= a.dims[n]; o += (int64_t)i * a.ostride[n]; }
+        }
         offr[r] = (int32_t)o;
     }
     for (int c = threadIdx.x; c < cols; c += blockDim.x) {
@@ -289,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 2) reconstruct_kernel(const ReconArg
             const Grid g = grid_of(gsel[gi] & 255u);
             if (threadIdx.x == 0) gsel[gi ^ 1] = ~0u;   // the slot after next is reset behind the next barrier
             gi ^= 1;
-            gemm(g, cur, ld, XS, R, prow, I * S, R, StoreLeft{nxt, nld, prow, I, prow});
+            gemm(g, cur, ld, XS, R, prow, I * S, R, StoreLeft{nxt, nld, prow, I, prow, a.lrev != 0});
             __syncthreads();                   // XS free, nxt complete
             cur = nxt;
             prow *= I;

@@ -319,6 +319,12 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
     a.cols = (int32_t)suf[best_k];
     a.lbuf = (int32_t)bl; a.t1 = (int32_t)bt1; a.rbuf = (int32_t)br; a.t2 = (int32_t)bt2;
     a.ldl = (int32_t)ldl(a.rows);
+    // 16-byte output stores need the output's stride-1 mode to be the fastest row index: mode 1 as enumerated,
+    // or the left block's last mode k with the rows enumerated big-endian
+    {
+        const int m1 = (perm ? perm[0] : 1) - 1;   // train mode with output stride 1
+        a.lrev = (m1 != 0 && m1 == best_k - 1) ? 1 : 0;
+    }
     for (int j = 0; j < best_k; ++j) a.ld[j] = (int32_t)ldl(pre[j + 1]);
     a.tm = (a.cols + 79) / 80 * 80 < (a.cols + 63) / 64 * 64 ? 5 : 4;   // 80 columns when that pads less
     for (int n = 0; n < N; ++n) { a.dims[n] = t->dims[n]; a.ostride[n] = ostride[n]; }
@@ -415,9 +421,45 @@ ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const f
     a.train_cap = cap;
     a.ranks = ranks_dev;
     const int64_t g = gmax;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (order >= 2 && gmax <= 32 && !std::getenv("TTC_TTSVD_FUSED")) {
+        // warp-per-eigenproblem pipeline; its workspace is stream-ordered (allocated and freed on `stream`)
+        const int64_t B = batch;
+        const size_t bz = sizeof(float) * (size_t)(B * total), bg = sizeof(double) * (size_t)(B * g * g);
+        const size_t bl = sizeof(double) * (size_t)(B * g), bo = sizeof(int32_t) * (size_t)(B * g);
+        const size_t bn = sizeof(double) * (size_t)B;
+        auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+        const size_t bytes = al(bz) + 2 * al(bg) + al(bl) + al(bo) + al(bn);
+        void* ws = nullptr;
+        static bool pool_kept = false;   // keep freed workspace in the device's default pool across calls
+        if (!pool_kept) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            pool_kept = true;
+        }
+        cudaError_t e = cudaMallocAsync(&ws, bytes, cs);
+        if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd workspace (cudaMallocAsync)");
+        char* p = static_cast<char*>(ws);
+        ttc::TtsvdWs w;
+        w.z = reinterpret_cast<float*>(p); p += al(bz);
+        w.g = reinterpret_cast<double*>(p); p += al(bg);
+        w.v = reinterpret_cast<double*>(p); p += al(bg);
+        w.lam = reinterpret_cast<double*>(p); p += al(bl);
+        w.ord = reinterpret_cast<int32_t*>(p); p += al(bo);
+        w.nrm = reinterpret_cast<double*>(p);
+        e = ttc::launch_ttsvd_pipeline(a, w, cs);
+        const cudaError_t ef = cudaFreeAsync(ws, cs);
+        if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd launch");
+        if (ef != cudaSuccess) return cuda_fail(ef, "ttc_tt_svd workspace free");
+        return TTC_OK;
+    }
     const size_t smem = sizeof(double) * (size_t)(2 * g * g + g + 2 * (g / 2 + 1) + 32) +
                         sizeof(int) * (size_t)(g + 2 * (g / 2 + 1) + 4) + 16 + sizeof(float) * 2 * (size_t)total;
-    const cudaError_t e = ttc::launch_ttsvd(a, smem, reinterpret_cast<cudaStream_t>(stream));
+    const cudaError_t e = ttc::launch_ttsvd(a, smem, cs);
     if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd launch");
     return TTC_OK;
 }

@@ -105,6 +105,7 @@ struct ReconArgs {
     int32_t  tm;                        // output tile 64 x 16 tm (tm = 4 or 5)
     int32_t  ldl;                       // row stride of Left^T (rows rounded up to a multiple of 4)
     int32_t  ld[TTC_MAX_ORDER];         // row stride of the left partial P_{j+1}^T (= ldl for j = k - 1)
+    int32_t  lrev;                      // 1: Left's rows enumerate modes k..1 fastest-first (big-endian)
     int32_t  dims[TTC_MAX_ORDER];
     int64_t  ostride[TTC_MAX_ORDER];    // output stride of train mode n (permuted Eq. 2 order)
     TrainDev t;
@@ -126,5 +127,15 @@ struct TtsvdArgs {
     int32_t* ranks;                     // device [B, N + 1]
 };
 cudaError_t launch_ttsvd(const TtsvdArgs& a, size_t smem_bytes, cudaStream_t s);
+// workspace of the multi-kernel TT-SVD (Gram sides <= 32): Z_n, the Gram matrix, its eigen-decomposition
+struct TtsvdWs {
+    float*   z;                         // B x elems
+    double*  g;                         // B x gmax^2
+    double*  v;                         // B x gmax^2
+    double*  lam;                       // B x gmax
+    int32_t* ord;                       // B x gmax
+    double*  nrm;                       // B
+};
+cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStream_t s);
 
 }  // namespace ttc

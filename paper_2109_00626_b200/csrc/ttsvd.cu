@@ -33,6 +33,50 @@ __device__ double block_sum(double v, double* red) {
     return t;
 }
 
+// Source offsets of X^rho's elements e = tid, tid + step, ... (Alg. 2 step 1's permutation as strides): the
+// mixed-radix digits of e are decomposed once, then advanced by the digits of `step` with carries (no integer
+// division per element).
+constexpr int kWalkMax = 16;   // orders up to 16 walk in registers (fully unrolled); larger ones divide
+struct GatherWalk {
+    int32_t dig[kWalkMax], sd[kWalkMax];
+    int64_t off;
+    int e, step;
+    __device__ __forceinline__ void init(const TtsvdArgs& a, int e0, int st) {
+        e = e0;
+        step = st;
+        off = 0;
+        if (a.N > kWalkMax) { off = slow(a, e); return; }
+        int q = e, r = step;
+#pragma unroll
+        for (int k = 0; k < kWalkMax; ++k)
+            if (k < a.N) {
+                dig[k] = q % a.dims[k]; q /= a.dims[k];
+                sd[k] = r % a.dims[k]; r /= a.dims[k];
+                off += (int64_t)dig[k] * a.in_stride[k];
+            }
+    }
+    __device__ __forceinline__ static int64_t slow(const TtsvdArgs& a, int e) {
+        int q = e;
+        int64_t o = 0;
+        for (int k = 0; k < a.N; ++k) { const int i = q % a.dims[k]; q /= a.dims[k]; o += (int64_t)i * a.in_stride[k]; }
+        return o;
+    }
+    __device__ __forceinline__ void next(const TtsvdArgs& a) {
+        e += step;
+        if (a.N > kWalkMax) { off = slow(a, e); return; }
+        int carry = 0;
+#pragma unroll
+        for (int k = 0; k < kWalkMax; ++k)
+            if (k < a.N) {
+                int d = dig[k] + sd[k] + carry;
+                carry = d >= a.dims[k];
+                if (carry) d -= a.dims[k];
+                off += (int64_t)(d - dig[k]) * a.in_stride[k];
+                dig[k] = d;
+            }
+    }
+};
+
 // Symmetric eigenproblem of G (n x n, row-major in shared memory, overwritten by the rotated matrix) by cyclic
 // Jacobi; V (n x n) receives the eigenvectors as columns.  Round-robin ordering: n' = n rounded up to even
 // players, n'/2 disjoint rotations per round (player n' - 1 is a dummy when n is odd), n' - 1 rounds a sweep.
@@ -120,11 +164,10 @@ __global__ void __launch_bounds__(kThreads) ttsvd_kernel(const TtsvdArgs a) {
     int32_t* rout = a.ranks + (int64_t)b * (N + 1);
     // ---- Z <- X^rho (mode k of X^rho is read with the source stride in_stride[k]); ||X||_F^2
     double nrm = 0.0;
-    for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
-        int q = e;
-        int64_t o = 0;
-        for (int k = 0; k < N; ++k) { const int i = q % a.dims[k]; q /= a.dims[k]; o += (int64_t)i * a.in_stride[k]; }
-        const float v = __ldg(src + o);
+    GatherWalk gw;
+    gw.init(a, threadIdx.x, blockDim.x);
+    for (int e = threadIdx.x; e < a.elems; e += blockDim.x, gw.next(a)) {
+        const float v = __ldg(src + gw.off);
         Z[e] = v;
         nrm += (double)v * v;
     }
@@ -229,12 +272,376 @@ __global__ void __launch_bounds__(kThreads) ttsvd_kernel(const TtsvdArgs a) {
     if (threadIdx.x == 0) rout[N] = 1;
 }
 
+// ===================================================================================================
+// Multi-kernel pipeline for Gram sides <= 32 (ttc_tt_svd's default; the fused kernel above keeps larger
+// sides): the per-tensor Jacobi iterations are latency chains (each round waits on one rotation's fp64
+// sqrt / divide), so instead of one CTA per tensor holding the whole SVD (3 per SM, the SM idle behind the
+// CTA barriers), every eigenproblem runs on ONE warp with no CTA barriers, 4 per CTA and up to 8 CTAs per
+// SM, the whole batch in flight at once; the dense phases (gather, Gram matrices, U, the next unfolding)
+// are separate CTA-per-tensor kernels, passing Z_n, the Gram matrix and its eigenvectors through a
+// workspace (L2-resident at A2's sizes).
+//   first  : Z_0 <- X^rho, ||X||^2, Gram of Z_0
+//   jacobi : (per step n) eigenvectors, eigenvalues in descending order, the delta-truncated rank R_n
+//   step   : (per step n) core n = U (R24 signs), Z_{n+1}, its Gram (or, after the last step, core N)
+
+// Gram matrix of Z (m x ncols, Z[r + m c]) of the smaller side, fp64, into g (side x side, row-major).
+// Rows side: a thread per entry (consecutive threads read consecutive rows of a column); columns side: a warp
+// per entry, lanes along the column (contiguous, conflict-free), shuffle-reduced.
+__device__ void gram_to(const float* Z, int m, int ncols, double* g) {
+    const bool rows_side = m <= ncols;
+    const int side = rows_side ? m : ncols;
+    if (rows_side) {
+        for (int e = threadIdx.x; e < side * side; e += blockDim.x) {
+            const int i = e / side, j = e - i * side;
+            if (j < i) continue;
+            double acc0 = 0.0, acc1 = 0.0;   // two chains: half the dependent-add latency
+            int c = 0;
+            for (; c + 1 < ncols; c += 2) {
+                acc0 += (double)Z[i + m * c] * Z[j + m * c];
+                acc1 += (double)Z[i + m * (c + 1)] * Z[j + m * (c + 1)];
+            }
+            if (c < ncols) acc0 += (double)Z[i + m * c] * Z[j + m * c];
+            g[i * side + j] = acc0 + acc1;
+            g[j * side + i] = acc0 + acc1;
+        }
+        return;
+    }
+    const int wp = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int e = wp; e < side * side; e += nw) {
+        const int i = e / side, j = e - i * side;
+        if (j < i) continue;
+        const float* zi = Z + m * i;
+        const float* zj = Z + m * j;
+        double acc = 0.0;
+        for (int r = l; r < m; r += 32) acc += (double)zi[r] * zj[r];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (l == 0) {
+            g[i * side + j] = acc;
+            g[j * side + i] = acc;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a, const TtsvdWs w) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    __shared__ int32_t rad[TTC_MAX_ORDER];
+    __shared__ int64_t dstr[TTC_MAX_ORDER];
+    double* red = reinterpret_cast<double*>(sraw);                // 32
+    float* Z = reinterpret_cast<float*>(red + 32);
+    const int b = blockIdx.x, N = a.N;
+    const float* src = a.dense + (int64_t)b * a.elems;
+    float* zg = w.z + (int64_t)b * a.elems;
+    // the source's modes in memory order (X^rho's modes sorted by source stride), with X^rho's compact strides:
+    // the source is read contiguously (coalesced) and scattered into Z in X^rho order
+    if (threadIdx.x == 0) {
+        int64_t cs = 1;
+        int64_t xs[TTC_MAX_ORDER];
+        for (int k = 0; k < N; ++k) { xs[k] = cs; cs *= a.dims[k]; }
+        for (int p = 0; p < N; ++p) {
+            int best = -1;
+            for (int k = 0; k < N; ++k) {
+                bool used = false;
+                for (int q = 0; q < p; ++q) used |= rad[q] == -1 - k;   // (temporarily: -1 - mode)
+                if (!used && (best < 0 || a.in_stride[k] < a.in_stride[best])) best = k;
+            }
+            rad[p] = -1 - best;
+        }
+        for (int p = 0; p < N; ++p) { const int k = -1 - rad[p]; rad[p] = a.dims[k]; dstr[p] = xs[k]; }
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    {
+        int dig[kWalkMax], sd[kWalkMax];
+        int64_t off = 0;
+        const bool fast = N <= kWalkMax;
+        if (fast) {
+            int q = threadIdx.x, r = blockDim.x;
+#pragma unroll
+            for (int p = 0; p < kWalkMax; ++p)
+                if (p < N) { dig[p] = q % rad[p]; q /= rad[p]; sd[p] = r % rad[p]; r /= rad[p]; off += dig[p] * dstr[p]; }
+        }
+        for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
+            if (!fast) {
+                int q = e;
+                off = 0;
+                for (int p = 0; p < N; ++p) { off += (q % rad[p]) * dstr[p]; q /= rad[p]; }
+            }
+            const float v = __ldg(src + e);
+            Z[off] = v;
+            nrm += (double)v * v;
+            if (fast) {
+                int carry = 0;
+#pragma unroll
+                for (int p = 0; p < kWalkMax; ++p)
+                    if (p < N) {
+                        int d = dig[p] + sd[p] + carry;
+                        carry = d >= rad[p];
+                        if (carry) d -= rad[p];
+                        off += (d - dig[p]) * dstr[p];
+                        dig[p] = d;
+                    }
+            }
+        }
+    }
+    nrm = block_sum(nrm, red);   // (its barriers also publish Z)
+    for (int e = threadIdx.x; e < a.elems; e += blockDim.x) zg[e] = Z[e];
+    if (threadIdx.x == 0) {
+        w.nrm[b] = nrm;
+        a.ranks[(int64_t)b * (N + 1)] = 1;
+    }
+    gram_to(Z, a.dims[0], a.elems / a.dims[0], w.g + (int64_t)b * a.gmax * a.gmax);
+}
+
+// Cyclic Jacobi of G (n x n, n <= 32) by one warp.  Same round-robin pairs and rotation rule as jacobi(); each
+// round applies all its rotations at once as 2 x 2 block updates G' = J_p^T G J_q (G double-buffered, so one
+// pass and no ordering between blocks) and V' = V J.  Returns the buffer holding the final G.
+__device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* cs, double* sn, int* pa, int* pb) {
+    const int lane = threadIdx.x & 31;
+    for (int e = lane; e < n * n; e += 32) V[e] = (e / n == e % n) ? 1.0 : 0.0;
+    const int np = (n + 1) & ~1, half = np / 2;
+    // index walks without divisions: e += 32 over (q1, q2) = (e / half, e % half) and (k, q) = (e / half, ...)
+    const int d1 = 32 / half, d2 = 32 - d1 * half;
+    const int k0 = lane / half, q0 = lane - k0 * half;
+    __syncwarp();
+    for (int sweep = 0; sweep < kSweeps; ++sweep) {
+        bool any = false;
+        // round-robin positions of this lane's two players (lane < half): players 1..np-1 rotate by one a round
+        int px = lane == 0 ? 0 : lane, py = np - 1 - lane;   // pos(j) at t = 0 is j
+        for (int t = 0; t < np - 1; ++t) {
+            bool rot = false;
+            if (lane < half) {
+                int x = px, y = py;
+                if (x > y) { const int u = x; x = y; y = u; }
+                double c = 1.0, s = 0.0;
+                if (y < n) {
+                    const double app = G[x * n + x], aqq = G[y * n + y], apq = G[x * n + y];
+                    if (fabs(apq) > 1e-300 && fabs(apq) > DBL_EPSILON * sqrt(fabs(app * aqq))) {
+                        const double th = (aqq - app) / (2.0 * apq);
+                        const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                        c = 1.0 / sqrt(tt * tt + 1.0);
+                        s = tt * c;
+                        rot = true;
+                    }
+                }
+                cs[lane] = c; sn[lane] = s; pa[lane] = x; pb[lane] = y;
+            }
+            // next round: players 1..np-1 advance one position (np - 1 wraps to 1); player 0 stays
+            if (px != 0) px = px == np - 1 ? 1 : px + 1;
+            py = py == np - 1 ? 1 : py + 1;
+            any |= __any_sync(0xffffffffu, rot);
+            __syncwarp();
+            int q1 = k0, q2 = q0;
+            for (int e = lane; e < half * half; e += 32) {   // block (pair q1 rows) x (pair q2 columns)
+                if (e != lane) { q1 += d1; q2 += d2; if (q2 >= half) { q2 -= half; ++q1; } }
+                const int a1 = pa[q1], b1 = pb[q1], a2 = pa[q2], b2 = pb[q2];
+                const double c1 = cs[q1], s1 = sn[q1], c2 = cs[q2], s2 = sn[q2];
+                const bool hb1 = b1 < n, hb2 = b2 < n;
+                const double g00 = G[a1 * n + a2], g01 = hb2 ? G[a1 * n + b2] : 0.0;
+                const double g10 = hb1 ? G[b1 * n + a2] : 0.0, g11 = hb1 && hb2 ? G[b1 * n + b2] : 0.0;
+                const double x00 = c2 * g00 - s2 * g01, x01 = s2 * g00 + c2 * g01;   // B J2
+                const double x10 = c2 * g10 - s2 * g11, x11 = s2 * g10 + c2 * g11;
+                Gn[a1 * n + a2] = c1 * x00 - s1 * x10;                               // J1^T (B J2)
+                if (hb2) Gn[a1 * n + b2] = c1 * x01 - s1 * x11;
+                if (hb1) Gn[b1 * n + a2] = s1 * x00 + c1 * x10;
+                if (hb1 && hb2) Gn[b1 * n + b2] = s1 * x01 + c1 * x11;
+            }
+            int k = k0, q = q0;
+            for (int e = lane; e < n * half; e += 32) {      // V J: row k, pair q
+                if (e != lane) { k += d1; q += d2; if (q >= half) { q -= half; ++k; } }
+                const int x = pa[q], y = pb[q];
+                if (y >= n || sn[q] == 0.0) continue;
+                const double c = cs[q], s = sn[q];
+                const double vx = V[k * n + x], vy = V[k * n + y];
+                V[k * n + x] = c * vx - s * vy;
+                V[k * n + y] = s * vx + c * vy;
+            }
+            __syncwarp();
+            double* tmp = G; G = Gn; Gn = tmp;
+        }
+        if (!any) break;
+    }
+    return G;
+}
+
+constexpr int kJacWarps = 4;
+
+__global__ void __launch_bounds__(32 * kJacWarps) ttsvd_jacobi_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * kJacWarps + warp;
+    if (b >= a.B) return;   // (warp-local from here on: no CTA barriers)
+    const int g2 = a.gmax * a.gmax, N = a.N;
+    double* G = reinterpret_cast<double*>(sraw) + (size_t)warp * (3 * g2 + 2 * 16 + 32);
+    double* Gn = G + g2;
+    double* V = Gn + g2;
+    double* cs = V + g2;
+    double* sn = cs + 16;
+    double* lam = sn + 16;                                   // 32
+    int* pa = reinterpret_cast<int*>(sraw + sizeof(double) * (size_t)kJacWarps * (3 * g2 + 2 * 16 + 32)) + warp * 96;
+    int* pb = pa + 16;
+    int* ord = pb + 16;                                      // 32
+    int* misc = ord + 32;                                    // [0]: R
+    int32_t* rk = a.ranks + (int64_t)b * (N + 1);
+    const int Rprev = rk[n];
+    int64_t cur = Rprev;
+    for (int k = n; k < N; ++k) cur *= a.dims[k];
+    const int m = Rprev * a.dims[n], ncols = (int)(cur / m), side = m <= ncols ? m : ncols;
+    const double* gsrc = w.g + (int64_t)b * g2;
+    for (int e = lane; e < side * side; e += 32) G[e] = gsrc[e];
+    __syncwarp();
+    const double* Gf = jacobi_warp(G, Gn, V, side, cs, sn, pa, pb);
+    // eigenvalues, descending stable order
+    if (lane < side) lam[lane] = fmax(Gf[lane * side + lane], 0.0);
+    __syncwarp();
+    if (lane < side) {
+        int rank = 0;
+        for (int i = 0; i < side; ++i) rank += (lam[i] > lam[lane]) || (lam[i] == lam[lane] && i < lane);
+        ord[rank] = lane;
+    }
+    __syncwarp();
+    if (lane == 0) {   // R23 / R25: the delta-truncated rank over the values above the floor
+        const double top = lam[ord[0]], delta2 = a.eps2 * w.nrm[b];
+        int keep = 0;
+        for (int j = 0; j < side; ++j) keep += lam[ord[j]] > kSigmaFloor * kSigmaFloor * top && top > 0.0;
+        int R = keep < 1 ? 1 : keep;
+        double tail = 0.0;
+        for (int j = keep - 1; j >= 1; --j) {
+            tail += lam[ord[j]];
+            if (tail <= delta2) R = j; else break;
+        }
+        rk[n + 1] = R;
+    }
+    double* vdst = w.v + (int64_t)b * g2;
+    for (int e = lane; e < side * side; e += 32) vdst[e] = V[e];
+    if (lane < side) {
+        w.lam[(int64_t)b * a.gmax + lane] = lam[lane];
+        w.ord[(int64_t)b * a.gmax + lane] = ord[lane];
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) ttsvd_step_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    const int b = blockIdx.x, N = a.N, gm = a.gmax;
+    const int32_t* rk = a.ranks + (int64_t)b * (N + 1);
+    const int Rprev = rk[n], R = rk[n + 1];
+    int64_t cur = Rprev;
+    for (int k = n; k < N; ++k) cur *= a.dims[k];
+    const int m = Rprev * a.dims[n], ncols = (int)(cur / m);
+    const bool rows_side = m <= ncols;
+    const int side = rows_side ? m : ncols;
+    double* V = reinterpret_cast<double*>(sraw);                  // gm x gm
+    double* lam = V + gm * gm;                                     // gm
+    int* ord = reinterpret_cast<int*>(lam + gm);                   // gm
+    int64_t* oo = reinterpret_cast<int64_t*>(ord + ((gm + 3) & ~3));   // [0]: offset of core n
+    float* Z = reinterpret_cast<float*>(oo + 2);
+    float* U = Z + a.elems;
+    if (threadIdx.x == 0) {
+        int64_t o = 0;
+        for (int k = 0; k < n; ++k) o += (int64_t)rk[k] * a.dims[k] * rk[k + 1];
+        oo[0] = o;
+    }
+    const float* zg = w.z + (int64_t)b * a.elems;
+    for (int e = threadIdx.x; e < (int)cur; e += blockDim.x) Z[e] = zg[e];
+    for (int e = threadIdx.x; e < side * side; e += blockDim.x) V[e] = w.v[(int64_t)b * gm * gm + e];
+    for (int j = threadIdx.x; j < side; j += blockDim.x) {
+        lam[j] = w.lam[(int64_t)b * gm + j];
+        ord[j] = w.ord[(int64_t)b * gm + j];
+    }
+    __syncthreads();
+    float* out = a.cores + (int64_t)b * a.train_cap + oo[0];
+    // ---- U (m x R)
+    if (rows_side) {
+        for (int e = threadIdx.x; e < m * R; e += blockDim.x) {
+            const int j = e / m, i = e - j * m;
+            U[e] = (float)V[i * side + ord[j]];
+        }
+    } else {
+        for (int e = threadIdx.x; e < m * R; e += blockDim.x) {
+            const int j = e / m, r = e - j * m;
+            const int col = ord[j];
+            double acc = 0.0;
+            for (int c = 0; c < ncols; ++c) acc += (double)Z[r + m * c] * V[c * side + col];
+            U[e] = lam[col] > 0.0 ? (float)(acc / sqrt(lam[col])) : 0.f;
+        }
+    }
+    __syncthreads();
+    // ---- R24: one warp per column, the largest |entry| (lowest row on ties) made positive
+    {
+        const int wp = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int j = wp; j < R; j += nw) {
+            const float* u = U + (int64_t)m * j;
+            float best = -1.f;
+            int bi = 0;
+            for (int i = l; i < m; i += 32) {
+                const float v = fabsf(u[i]);
+                if (v > best) { best = v; bi = i; }
+            }
+            for (int o2 = 16; o2 > 0; o2 >>= 1) {
+                const float ob = __shfl_xor_sync(0xffffffffu, best, o2);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o2);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (l == 0 && u[bi] < 0.f) lam[ord[j]] = -lam[ord[j]];   // sign bit carries the flip (lam may be 0)
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * R; e += blockDim.x) {
+        const int j = e / m;
+        out[e] = signbit(lam[ord[j]]) ? -U[e] : U[e];
+    }
+    __syncthreads();
+    // ---- Z_{n+1} = U^T Z (rows side) or S_R V_R^T (cols side), signs applied; into U's buffer
+    for (int e = threadIdx.x; e < R * ncols; e += blockDim.x) {
+        const int c = e / R, j = e - c * R;
+        const int col = ord[j];
+        const double sgn = signbit(lam[col]) ? -1.0 : 1.0;
+        double v;
+        if (rows_side) {
+            double acc = 0.0;
+            for (int i = 0; i < m; ++i) acc += V[i * side + col] * (double)Z[i + m * c];
+            v = sgn * acc;
+        } else {
+            v = sgn * sqrt(fabs(lam[col])) * V[c * side + col];
+        }
+        U[j + R * c] = (float)v;
+    }
+    __syncthreads();
+    const int nel = R * ncols;
+    if (n + 2 == N) {   // the last core G^(N) = Z_{N-1}
+        for (int e = threadIdx.x; e < nel; e += blockDim.x) out[(int64_t)m * R + e] = U[e];
+        if (threadIdx.x == 0) a.ranks[(int64_t)b * (N + 1) + N] = 1;
+        return;
+    }
+    float* zo = w.z + (int64_t)b * a.elems;
+    for (int e = threadIdx.x; e < nel; e += blockDim.x) zo[e] = U[e];
+    const int m2 = R * a.dims[n + 1];
+    gram_to(U, m2, nel / m2, w.g + (int64_t)b * gm * gm);
+}
+
 }  // namespace
 
 cudaError_t launch_ttsvd(const TtsvdArgs& a, size_t smem_bytes, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(ttsvd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
     ttsvd_kernel<<<a.B, kThreads, smem_bytes, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStream_t s) {
+    const int gm = a.gmax;
+    const size_t smem_first = sizeof(double) * 32 + sizeof(float) * (size_t)a.elems;
+    const size_t smem_jac = (sizeof(double) * (size_t)(3 * gm * gm + 2 * 16 + 32) + sizeof(int) * 96) * kJacWarps;
+    const size_t smem_step = sizeof(double) * (size_t)(gm * gm + gm) + sizeof(int) * (size_t)((gm + 3) & ~3) +
+                             2 * sizeof(int64_t) + 2 * sizeof(float) * (size_t)a.elems;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(ttsvd_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_first)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(ttsvd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_jac)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(ttsvd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_step)) != cudaSuccess) return e;
+    ttsvd_first_kernel<<<a.B, kThreads, smem_first, s>>>(a, w);
+    for (int n = 0; n + 1 < a.N; ++n) {
+        ttsvd_jacobi_kernel<<<(a.B + kJacWarps - 1) / kJacWarps, 32 * kJacWarps, smem_jac, s>>>(a, w, n);
+        ttsvd_step_kernel<<<a.B, kThreads, smem_step, s>>>(a, w, n);
+    }
     return cudaGetLastError();
 }
 
