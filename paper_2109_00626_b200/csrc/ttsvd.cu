@@ -322,10 +322,60 @@ __device__ void gram_to(const float* Z, int m, int ncols, double* g) {
     }
 }
 
+// The same Gram matrix as register-tiled fp64 products: 4 x 4 tiles of the upper triangle, the summed index
+// split into chunks so that every thread has a (tile, chunk) item; partial tiles added into gs (shared, side^2
+// doubles) with shared-memory atomics, then gs (mirrored) written to g.  Element (i, t) of the side x len
+// operand is Z[i si + t st].
+__device__ void gram_tiled(const float* Z, int m, int ncols, double* gs, double* g) {
+    const bool rows_side = m <= ncols;
+    const int side = rows_side ? m : ncols, len = rows_side ? ncols : m;
+    const int si = rows_side ? 1 : m, st = rows_side ? m : 1;
+    const int T = (side + 3) >> 2, pairs = T * (T + 1) / 2;
+    const int chunks = max(1, min(len, (int)blockDim.x / pairs)), clen = (len + chunks - 1) / chunks;
+    for (int e = threadIdx.x; e < side * side; e += blockDim.x) gs[e] = 0.0;
+    __syncthreads();
+    for (int it = threadIdx.x; it < pairs * chunks; it += blockDim.x) {
+        const int ch = it / pairs;
+        int p = it - ch * pairs, ti = 0;
+        while (p >= T - ti) { p -= T - ti; ++ti; }   // upper-triangle tile (ti, tj), tj >= ti
+        const int tj = ti + p, i0 = 4 * ti, j0 = 4 * tj;
+        const int t0 = ch * clen, t1 = min(len, t0 + clen);
+        double acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+        int ia[4], ja[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { ia[u] = min(i0 + u, side - 1) * si; ja[u] = min(j0 + u, side - 1) * si; }
+        for (int t = t0; t < t1; ++t) {
+            const float* zt = Z + t * st;
+            double x[4], y[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { x[u] = zt[ia[u]]; y[u] = zt[ja[u]]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(x[u], y[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (i0 + u < side && j0 + v < side) atomicAdd(&gs[(i0 + u) * side + j0 + v], acc[u][v]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < side * side; e += blockDim.x) {
+        const int i = e / side, j = e - i * side;
+        // tiles cover (i, j) with tile(i) <= tile(j); the rest mirror
+        g[e] = (i >> 2) <= (j >> 2) ? gs[e] : gs[j * side + i];
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a, const TtsvdWs w) {
     extern __shared__ __align__(16) unsigned char sraw[];
     __shared__ int32_t rad[TTC_MAX_ORDER];
-    __shared__ int64_t dstr[TTC_MAX_ORDER];
+    __shared__ int32_t dstr[TTC_MAX_ORDER];
     double* red = reinterpret_cast<double*>(sraw);                // 32
     float* Z = reinterpret_cast<float*>(red + 32);
     const int b = blockIdx.x, N = a.N;
@@ -346,13 +396,13 @@ __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a
             }
             rad[p] = -1 - best;
         }
-        for (int p = 0; p < N; ++p) { const int k = -1 - rad[p]; rad[p] = a.dims[k]; dstr[p] = xs[k]; }
+        for (int p = 0; p < N; ++p) { const int k = -1 - rad[p]; rad[p] = a.dims[k]; dstr[p] = (int32_t)xs[k]; }
     }
     __syncthreads();
     double nrm = 0.0;
     {
         int dig[kWalkMax], sd[kWalkMax];
-        int64_t off = 0;
+        int off = 0;   // (elems <= 16384)
         const bool fast = N <= kWalkMax;
         if (fast) {
             int q = threadIdx.x, r = blockDim.x;
@@ -389,7 +439,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a
         w.nrm[b] = nrm;
         a.ranks[(int64_t)b * (N + 1)] = 1;
     }
-    gram_to(Z, a.dims[0], a.elems / a.dims[0], w.g + (int64_t)b * a.gmax * a.gmax);
+    gram_tiled(Z, a.dims[0], a.elems / a.dims[0], red + 32 + ((a.elems + 1) >> 1), w.g + (int64_t)b * a.gmax * a.gmax);
 }
 
 // Cyclic Jacobi of G (n x n, n <= 32) by one warp.  Same round-robin pairs and rotation rule as jacobi(); each
@@ -519,7 +569,7 @@ __global__ void __launch_bounds__(32 * kJacWarps) ttsvd_jacobi_kernel(const Ttsv
     }
 }
 
-__global__ void __launch_bounds__(kThreads) ttsvd_step_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
+__global__ void __launch_bounds__(kThreads, 3) ttsvd_step_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
     extern __shared__ __align__(16) unsigned char sraw[];
     const int b = blockIdx.x, N = a.N, gm = a.gmax;
     const int32_t* rk = a.ranks + (int64_t)b * (N + 1);
@@ -591,19 +641,41 @@ __global__ void __launch_bounds__(kThreads) ttsvd_step_kernel(const TtsvdArgs a,
     }
     __syncthreads();
     // ---- Z_{n+1} = U^T Z (rows side) or S_R V_R^T (cols side), signs applied; into U's buffer
-    for (int e = threadIdx.x; e < R * ncols; e += blockDim.x) {
-        const int c = e / R, j = e - c * R;
-        const int col = ord[j];
-        const double sgn = signbit(lam[col]) ? -1.0 : 1.0;
-        double v;
-        if (rows_side) {
-            double acc = 0.0;
-            for (int i = 0; i < m; ++i) acc += V[i * side + col] * (double)Z[i + m * c];
-            v = sgn * acc;
-        } else {
-            v = sgn * sqrt(fabs(lam[col])) * V[c * side + col];
+    if (rows_side) {   // U^T Z in 4 (j) x 4 (c) register tiles, fp64 accumulation
+        const int tj = (R + 3) >> 2, tc = (ncols + 3) >> 2;
+        for (int it = threadIdx.x; it < tj * tc; it += blockDim.x) {
+            const int c0 = 4 * (it / tj), j0 = 4 * (it - (it / tj) * tj);
+            int col[4], cc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { col[u] = ord[min(j0 + u, R - 1)]; cc[u] = m * min(c0 + u, ncols - 1); }
+            double acc[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+            for (int i = 0; i < m; ++i) {
+                double x[4], y[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { x[u] = V[i * side + col[u]]; y[u] = Z[i + cc[u]]; }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = fma(x[u], y[v], acc[u][v]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    if (j0 + u < R && c0 + v < ncols)
+                        U[j0 + u + R * (c0 + v)] = (float)(signbit(lam[col[u]]) ? -acc[u][v] : acc[u][v]);
         }
-        U[j + R * c] = (float)v;
+    } else {
+        for (int e = threadIdx.x; e < R * ncols; e += blockDim.x) {
+            const int c = e / R, j = e - c * R;
+            const int col = ord[j];
+            const double sgn = signbit(lam[col]) ? -1.0 : 1.0;
+            U[j + R * c] = (float)(sgn * sqrt(fabs(lam[col])) * V[c * side + col]);
+        }
     }
     __syncthreads();
     const int nel = R * ncols;
@@ -615,7 +687,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_step_kernel(const TtsvdArgs a,
     float* zo = w.z + (int64_t)b * a.elems;
     for (int e = threadIdx.x; e < nel; e += blockDim.x) zo[e] = U[e];
     const int m2 = R * a.dims[n + 1];
-    gram_to(U, m2, nel / m2, w.g + (int64_t)b * gm * gm);
+    gram_tiled(U, m2, nel / m2, V, w.g + (int64_t)b * gm * gm);   // (V is free by now)
 }
 
 }  // namespace
@@ -629,7 +701,7 @@ cudaError_t launch_ttsvd(const TtsvdArgs& a, size_t smem_bytes, cudaStream_t s) 
 
 cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStream_t s) {
     const int gm = a.gmax;
-    const size_t smem_first = sizeof(double) * 32 + sizeof(float) * (size_t)a.elems;
+    const size_t smem_first = sizeof(double) * (32 + (size_t)gm * gm) + sizeof(double) * (size_t)((a.elems + 1) / 2);
     const size_t smem_jac = (sizeof(double) * (size_t)(3 * gm * gm + 2 * 16 + 32) + sizeof(int) * 96) * kJacWarps;
     const size_t smem_step = sizeof(double) * (size_t)(gm * gm + gm) + sizeof(int) * (size_t)((gm + 3) & ~3) +
                              2 * sizeof(int64_t) + 2 * sizeof(float) * (size_t)a.elems;
