@@ -452,6 +452,15 @@ __device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* 
     // index walks without divisions: e += 32 over (q1, q2) = (e / half, e % half) and (k, q) = (e / half, ...)
     const int d1 = 32 / half, d2 = 32 - d1 * half;
     const int k0 = lane / half, q0 = lane - k0 * half;
+    // this lane's upper-triangle blocks e = lane + 32 u < half (half + 1) / 2 (<= 5 for half <= 16): q1 << 8 | q2
+    int bp[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+        int p = lane + 32 * u, q1 = 0;
+        if (p >= half * (half + 1) / 2) { bp[u] = -1; continue; }
+        while (p >= half - q1) { p -= half - q1; ++q1; }
+        bp[u] = (q1 << 8) | (q1 + p);
+    }
     __syncwarp();
     for (int sweep = 0; sweep < kSweeps; ++sweep) {
         bool any = false;
@@ -480,9 +489,10 @@ __device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* 
             py = py == np - 1 ? 1 : py + 1;
             any |= __any_sync(0xffffffffu, rot);
             __syncwarp();
-            int q1 = k0, q2 = q0;
-            for (int e = lane; e < half * half; e += 32) {   // block (pair q1 rows) x (pair q2 columns)
-                if (e != lane) { q1 += d1; q2 += d2; if (q2 >= half) { q2 -= half; ++q1; } }
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {   // upper-triangle blocks q1 <= q2 (G symmetric: the mirror is the transpose)
+                if (bp[u] < 0) break;
+                const int q1 = bp[u] >> 8, q2 = bp[u] & 255;
                 const int a1 = pa[q1], b1 = pb[q1], a2 = pa[q2], b2 = pb[q2];
                 const double c1 = cs[q1], s1 = sn[q1], c2 = cs[q2], s2 = sn[q2];
                 const bool hb1 = b1 < n, hb2 = b2 < n;
@@ -490,10 +500,13 @@ __device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* 
                 const double g10 = hb1 ? G[b1 * n + a2] : 0.0, g11 = hb1 && hb2 ? G[b1 * n + b2] : 0.0;
                 const double x00 = c2 * g00 - s2 * g01, x01 = s2 * g00 + c2 * g01;   // B J2
                 const double x10 = c2 * g10 - s2 * g11, x11 = s2 * g10 + c2 * g11;
-                Gn[a1 * n + a2] = c1 * x00 - s1 * x10;                               // J1^T (B J2)
-                if (hb2) Gn[a1 * n + b2] = c1 * x01 - s1 * x11;
-                if (hb1) Gn[b1 * n + a2] = s1 * x00 + c1 * x10;
-                if (hb1 && hb2) Gn[b1 * n + b2] = s1 * x01 + c1 * x11;
+                const double y00 = c1 * x00 - s1 * x10, y01 = c1 * x01 - s1 * x11;   // J1^T (B J2)
+                const double y10 = s1 * x00 + c1 * x10, y11 = s1 * x01 + c1 * x11;
+                Gn[a1 * n + a2] = y00;
+                Gn[a2 * n + a1] = y00;
+                if (hb2) { Gn[a1 * n + b2] = y01; Gn[b2 * n + a1] = y01; }
+                if (hb1) { Gn[b1 * n + a2] = y10; Gn[a2 * n + b1] = y10; }
+                if (hb1 && hb2) { Gn[b1 * n + b2] = y11; Gn[b2 * n + b1] = y11; }
             }
             int k = k0, q = q0;
             for (int e = lane; e < n * half; e += 32) {      // V J: row k, pair q
