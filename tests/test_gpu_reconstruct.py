@@ -114,3 +114,16 @@ def test_reconstruct_errors():
     with pytest.raises(ttc.TTCError) as e:
         ttc.ttc_reconstruct(TD, [1, 1, 2, 3])
     assert e.value.status == ttc.TTC_ERR_MODES
+
+
+@pytest.mark.parametrize("N,perm_first", [(4, 2), (4, 1), (5, 3), (6, 3), (3, 2)])
+def test_output_stride_one_mode_placement(N, perm_first):
+    """The output's stride-1 mode is the left block's first mode (little-endian rows), its last mode k (rows
+    enumerated big-endian, 16-byte stores) or elsewhere (scalar stores): all three give Eq. 9 + permutation."""
+    rng = np.random.default_rng(100 + 10 * N + perm_first)
+    dims = tuple(int(x) for x in rng.integers(3, 9, size=N))
+    r = np.stack([[1] + [int(x) for x in rng.choice([4, 8, 5], size=N - 1)] + [1] for _ in range(3)]).astype(np.int32)
+    T = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, r, dims, "geo")
+    rest = [k for k in range(1, N + 1) if k != perm_first]
+    perm = [perm_first] + list(rng.permutation(rest))
+    _check(T, _recon(T, perm), perm)

@@ -122,3 +122,24 @@ def test_ttsvd_errors():
     with pytest.raises(ttc.TTCError) as e:
         ttc.ttc_tt_svd_capacity((4, 5), perm=[1, 1])
     assert e.value.status == ttc.TTC_ERR_MODES
+
+
+@pytest.mark.parametrize("dims,eps", [((3, 4, 5), 0.0), ((20, 20, 20), 0.0), ((6, 5, 7, 4), 0.2), ((2, 3, 4, 3, 2), 0.1)])
+def test_pipeline_matches_fused_kernel(dims, eps, monkeypatch):
+    """The launch pipeline (one-warp Jacobi per eigenproblem, Gram sides <= 32) and the fused one-CTA-per-tensor
+    kernel (TTC_TTSVD_FUSED=1) implement the same Alg. 1 with the same readings: equal ranks, cores equal to
+    fp32 rounding (both stop Jacobi at the same rotation threshold; rotation order differs)."""
+    rng = np.random.default_rng(len(dims) + int(10 * eps))
+    Xs = [rng.standard_normal(dims) for _ in range(5)]
+    dense = _dense_batch(Xs)
+    T_pipe = ttc.ttc_tt_svd(dense, dims, eps)
+    monkeypatch.setenv("TTC_TTSVD_FUSED", "1")
+    T_fused = ttc.ttc_tt_svd(dense, dims, eps)
+    monkeypatch.delenv("TTC_TTSVD_FUSED")
+    for b, (cp, cf) in enumerate(zip(_trains(T_pipe), _trains(T_fused))):
+        assert [c.shape for c in cp] == [c.shape for c in cf], f"tensor {b}: ranks differ"
+        scale = np.linalg.norm(Xs[b])
+        for p, f in zip(cp, cf):
+            assert np.max(np.abs(p - f)) <= 1e-4 * max(1.0, scale), f"tensor {b}: cores differ"
+        err = np.linalg.norm(ref.dense_from_tt(cp) - Xs[b]) / scale
+        assert err <= max(eps, 2e-5) * (1 + 1e-4)
