@@ -241,6 +241,7 @@ def main():
         X, Y = ttgen.config_batch(cfg, "iid", b0, B, args.seed, dev)
         XD, YD = ttc.TTDevice.from_batch(X), ttc.TTDevice.from_batch(Y)
     stream = torch.cuda.current_stream(dev)
+    launches_per_step = 1   # kernels of ours per step (counted per op below where it differs)
 
     if cfg == "C3":
         plan = ttc.ttc_contract_plan_create(XD, YD, c["x_modes"], c["y_modes"])
@@ -293,6 +294,16 @@ def main():
             ttc.ttc_contract(plan, TX, TY, out=zc, stream=stream)
             ttc.ttc_reconstruct(ZD, plan.perm, out=out, stream=stream)
         kernel_name = "alg2 pipeline (ttsvd x2, splice, reconstruct)"
+        # launches per step: ttc_tt_svd is 1 + 2 (N - 1) launches when every Gram side is <= 32 (the warp-Jacobi
+        # pipeline, ttsvd.cu) else 1 fused launch; then the splice and the reconstruction
+        dims_full = [c["I"]] * c["N"]
+        side = 0
+        for n in range(c["N"] - 1):
+            left = int(np.prod(dims_full[:n + 1]))
+            right = int(np.prod(dims_full[n + 1:]))
+            side = max(side, min(left, right))
+        per_svd = 1 + 2 * (c["N"] - 1) if side <= 32 else 1
+        launches_per_step = 2 * per_svd + 2
     elif c["op"] == "reconstruct":
         n_el = c["I"] ** c["N"]
         out = torch.empty(B * n_el, dtype=torch.float32, device=dev)
@@ -427,7 +438,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "ours", "config": conf,
-                "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": args.steps,
+                "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": args.steps * launches_per_step,
                 "clocks": clk, "wall_s_timed_region": t_wall,
                 "per_step_ms": {"min": min(per_step_ms), "median": statistics.median(per_step_ms),
                                 "max": max(per_step_ms)}}
