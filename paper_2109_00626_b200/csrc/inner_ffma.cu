@@ -196,7 +196,11 @@ __device__ __forceinline__ void gemm_rows(const float* A, int sA, const float* B
 // out = A B^T over rows < 8 TA and columns < 4 ncols (ncols even); one dispatch on the row count per GEMM.
 __device__ __noinline__ void ff_gemm(const float* A, int sA, const float* B, int sB, int K, int TA, int ncols,
                                      float* out, int rs, int cs, int ci, unsigned idiv, int lane) {
-    const int lg = lane >> 2, lf = lane & 3;
+    // lane -> (row group lg, column group lf): lg from lane bits 1-3, lf from bits 0 and 4.  An LDS.128 costs one
+    // shared-memory wavefront per half-warp only when each half-warp's addresses come in runs of adjacent lanes
+    // or alternate lane by lane (tools/lds_bench.cu: lane >> 2 -> 2 wavefronts, lane & 3 -> 4); this mapping
+    // gives 2 for both the A (row) and the B (column) loads (lg = lane >> 2, lf = lane & 3: 2 and 4).
+    const int lg = (lane >> 1) & 7, lf = (lane & 1) | ((lane >> 4) << 1);
     A += lg * sA;
     if (TA >= 3) {
         if (TA == 4) gemm_rows<4>(A, sA, B, sB, K, ncols, out, rs, cs, ci, idiv, lg, lf);
