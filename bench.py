@@ -280,6 +280,8 @@ def main():
         out = torch.empty(B * n_out, dtype=torch.float32, device=dev)
         rk_x = torch.empty_like(rx_dev)
         rk_y = torch.empty_like(ry_dev)
+        ws_x = torch.empty(max(16, ttc.ttc_tt_svd_workspace(B, shape, px)), dtype=torch.uint8, device=dev)
+        ws_y = torch.empty(max(16, ttc.ttc_tt_svd_workspace(B, shape, py)), dtype=torch.uint8, device=dev)
         n_in = c["I"] ** c["N"]
         train_x = int(sum(int(a) * int(i) * int(b2) for a, i, b2 in
                           zip(TX.rank_rows()[0][:-1], TX.dims_np, TX.rank_rows()[0][1:])))
@@ -289,8 +291,8 @@ def main():
         alg_flops = 2.0 * B * (svd_mac + I * R1 * R1 + R1 * R1 * I * R1 + n_out * R1 + 2 * I * I * R1 * R1)
 
         def step():
-            ttc.ttc_tt_svd_into(X, shape, c["eps"], TX.cores, rk_x, perm=px, stream=stream)
-            ttc.ttc_tt_svd_into(Y, shape, c["eps"], TY.cores, rk_y, perm=py, stream=stream)
+            ttc.ttc_tt_svd_into(X, shape, c["eps"], TX.cores, rk_x, perm=px, stream=stream, workspace=ws_x)
+            ttc.ttc_tt_svd_into(Y, shape, c["eps"], TY.cores, rk_y, perm=py, stream=stream, workspace=ws_y)
             ttc.ttc_contract(plan, TX, TY, out=zc, stream=stream)
             ttc.ttc_reconstruct(ZD, plan.perm, out=out, stream=stream)
         kernel_name = "alg2 pipeline (ttsvd x2, splice, reconstruct)"

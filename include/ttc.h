@@ -175,12 +175,20 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
  *   ttc_tt_svd_capacity (the floats of the largest possible ranks R_n <= min(prod_{k<=n} I_k, prod_{k>n} I_k));
  *   ranks_dev: device int32 [B, N + 1], the ranks found (read them back before describing the trains in a
  *   ttc_tt_batch with offsets b * train_cap).
- * One CTA per tensor holds the tensor in shared memory: prod(dims) <= 16384 and every unfolding's smaller side
- * <= 64 (else TTC_ERR_UNSUPPORTED).  eps < 0: TTC_ERR_ARG.
+ *   workspace_dev / workspace_bytes: caller-owned device scratch (16-byte aligned) of at least the size
+ *   ttc_tt_svd_workspace returns.  With it, and every unfolding's smaller side <= 32, the decomposition runs as
+ *   a pipeline of 1 + 2 (N - 1) launches (one warp per eigenproblem); with NULL / too small a workspace, or
+ *   larger sides, as one fused launch (one CTA per tensor).  Both give the same ranks and cores to fp32
+ *   rounding.  The library allocates nothing.
+ * The tensor is held in shared memory: prod(dims) <= 16384 and every unfolding's smaller side <= 64 (else
+ * TTC_ERR_UNSUPPORTED).  eps < 0: TTC_ERR_ARG.
  * ------------------------------------------------------------------------------------------------- */
 ttc_status ttc_tt_svd_capacity(int32_t order, const int32_t* dims, const int32_t* perm, int64_t* train_cap);
+ttc_status ttc_tt_svd_workspace(int32_t batch, int32_t order, const int32_t* dims, const int32_t* perm,
+                                int64_t* workspace_bytes);   /* 0 when the fused launch is used anyway */
 ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const float* dense_dev, const int32_t* perm,
-                      double eps, float* cores_dev, int32_t* ranks_dev, void* stream);
+                      double eps, float* cores_dev, int32_t* ranks_dev, void* workspace_dev, int64_t workspace_bytes,
+                      void* stream);
 
 /* ---------------------------------------------------------------------------------------------------
  * Host cost model and batch partitioner (multi-GPU sharding).

@@ -34,7 +34,7 @@ TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG 
 TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
 
 EXPORTED = ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
-            "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity", "ttc_tt_svd", "ttc_tt_svd_capacity",
+            "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity", "ttc_tt_svd_workspace",
             "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
             "ttc_last_error", "ttc_version")
 
@@ -66,11 +66,14 @@ _lib.ttc_last_error.restype = ctypes.c_char_p
 _lib.ttc_version.restype = ctypes.c_int32
 _lib.ttc_reconstruct.argtypes = [_P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 _lib.ttc_tt_svd_capacity.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_tt_svd_workspace.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p]
 _lib.ttc_tt_svd.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                            ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+                            ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                            ctypes.c_void_p]
 for _f in ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
            "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity",
-           "ttc_contract", "ttc_pair_cost", "ttc_partition"):
+           "ttc_tt_svd_workspace", "ttc_contract", "ttc_pair_cost", "ttc_partition"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -302,16 +305,35 @@ def ttc_tt_svd_capacity(dims, perm=None) -> int:
     return cap.value
 
 
+def ttc_tt_svd_workspace(B: int, dims, perm=None) -> int:
+    """Bytes of device workspace ttc_tt_svd's launch pipeline needs for B tensors (0: the fused launch is used)."""
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
+    pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    nb = ctypes.c_int64(0)
+    _check(_lib.ttc_tt_svd_workspace(int(B), int(d.size), _ptr(d), _ptr(pm), ctypes.byref(nb)))
+    return nb.value
+
+
+def _svd_workspace(B, d, pm, device, workspace):
+    if workspace is not None:
+        return workspace
+    nb = ttc_tt_svd_workspace(B, d, pm)
+    return torch.empty(max(nb, 16), dtype=torch.uint8, device=device) if nb else None
+
+
 def ttc_tt_svd_into(dense: torch.Tensor, dims, eps: float, cores: torch.Tensor, ranks: torch.Tensor, perm=None,
-                    stream=None) -> None:
+                    stream=None, workspace: torch.Tensor = None) -> None:
     """ttc_tt_svd into caller-owned device buffers (no host synchronisation): cores float32 [B * capacity],
-    ranks int32 [B, N + 1]."""
+    ranks int32 [B, N + 1]; workspace: uint8 device scratch of ttc_tt_svd_workspace bytes (allocated here from
+    torch's caching allocator when None)."""
     d = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
     pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
     n_el = int(np.prod(d.astype(np.int64)))
     B = dense.numel() // max(n_el, 1)
+    ws = _svd_workspace(B, d, pm, dense.device, workspace)
     _check(_lib.ttc_tt_svd(int(B), int(d.size), _ptr(d), _ptr(dense) if dense.numel() else None, _ptr(pm),
-                           float(eps), _ptr(cores), _ptr(ranks), _stream_handle(stream)))
+                           float(eps), _ptr(cores), _ptr(ranks), _ptr(ws) if ws is not None else None,
+                           int(ws.numel()) if ws is not None else 0, _stream_handle(stream)))
 
 
 def ttc_tt_svd(dense: torch.Tensor, dims, eps: float, perm=None, stream=None) -> "TTDevice":
@@ -325,8 +347,10 @@ def ttc_tt_svd(dense: torch.Tensor, dims, eps: float, perm=None, stream=None) ->
     cap = ttc_tt_svd_capacity(d, pm)
     cores = torch.zeros(max(B * cap, 1), dtype=torch.float32, device=dense.device)
     ranks = torch.zeros((max(B, 1), d.size + 1), dtype=torch.int32, device=dense.device)
+    ws = _svd_workspace(B, d, pm, dense.device, None)
     _check(_lib.ttc_tt_svd(int(B), int(d.size), _ptr(d), _ptr(dense) if dense.numel() else None, _ptr(pm),
-                           float(eps), _ptr(cores), _ptr(ranks), _stream_handle(stream)))
+                           float(eps), _ptr(cores), _ptr(ranks), _ptr(ws) if ws is not None else None,
+                           int(ws.numel()) if ws is not None else 0, _stream_handle(stream)))
     rdims = d if pm is None else d[pm - 1]
     r = ranks[:B].cpu().numpy()
     return TTDevice(cores, rdims, ranks=r, offsets=np.arange(B, dtype=np.int64) * cap)

@@ -394,8 +394,38 @@ ttc_status ttc_tt_svd_capacity(int32_t order, const int32_t* dims, const int32_t
     return ttsvd_shape(order, dims, perm, &rd, &st, train_cap, &g);
 }
 
+namespace {
+// Byte layout of the TT-SVD pipeline's workspace (ttsvd.cu TtsvdWs): Z_n, Gram, eigenvectors, eigenvalues, order,
+// norms, each 256-byte aligned.  Returns the total.
+int64_t ttsvd_ws_layout(int64_t B, int64_t elems, int64_t g, int64_t* off) {
+    auto al = [](int64_t v) { return (v + 255) & ~int64_t(255); };
+    const int64_t sz[6] = {4 * B * elems, 8 * B * g * g, 8 * B * g * g, 8 * B * g, 4 * B * g, 8 * B};
+    int64_t o = 0;
+    for (int k = 0; k < 6; ++k) { off[k] = o; o += al(sz[k]); }
+    return o;
+}
+}  // namespace
+
+ttc_status ttc_tt_svd_workspace(int32_t batch, int32_t order, const int32_t* dims, const int32_t* perm,
+                                int64_t* workspace_bytes) {
+    g_last_error.clear();
+    if (!workspace_bytes) return fail(TTC_ERR_NULL, "workspace_bytes is NULL");
+    if (batch < 0) return fail(TTC_ERR_ARG, "batch = %d < 0", batch);
+    std::vector<int32_t> rd;
+    std::vector<int64_t> st;
+    int64_t cap;
+    int32_t gmax;
+    ttc_status s;
+    if ((s = ttsvd_shape(order, dims, perm, &rd, &st, &cap, &gmax)) != TTC_OK) return s;
+    int64_t total = 1, off[6];
+    for (int n = 0; n < order; ++n) total *= rd[n];
+    *workspace_bytes = (order >= 2 && gmax <= 32) ? ttsvd_ws_layout(batch, total, gmax, off) : 0;
+    return TTC_OK;
+}
+
 ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const float* dense_dev, const int32_t* perm,
-                      double eps, float* cores_dev, int32_t* ranks_dev, void* stream) {
+                      double eps, float* cores_dev, int32_t* ranks_dev, void* workspace_dev, int64_t workspace_bytes,
+                      void* stream) {
     g_last_error.clear();
     if (batch < 0) return fail(TTC_ERR_ARG, "batch = %d < 0", batch);
     if (!(eps >= 0.0)) return fail(TTC_ERR_ARG, "eps = %g must be >= 0", eps);
@@ -409,6 +439,7 @@ ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const f
     if (!dense_dev || !cores_dev || !ranks_dev) return fail(TTC_ERR_NULL, "dense_dev / cores_dev / ranks_dev is NULL");
     if ((reinterpret_cast<uintptr_t>(dense_dev) | reinterpret_cast<uintptr_t>(cores_dev)) & 3u)
         return fail(TTC_ERR_ALIGN, "dense_dev / cores_dev not 4-byte aligned");
+    if (reinterpret_cast<uintptr_t>(workspace_dev) & 15u) return fail(TTC_ERR_ALIGN, "workspace_dev not 16-byte aligned");
     ttc::TtsvdArgs a;
     std::memset(&a, 0, sizeof(a));
     a.B = batch; a.N = order; a.gmax = gmax;
@@ -422,39 +453,20 @@ ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const f
     a.ranks = ranks_dev;
     const int64_t g = gmax;
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-    if (order >= 2 && gmax <= 32 && !std::getenv("TTC_TTSVD_FUSED")) {
-        // warp-per-eigenproblem pipeline; its workspace is stream-ordered (allocated and freed on `stream`)
-        const int64_t B = batch;
-        const size_t bz = sizeof(float) * (size_t)(B * total), bg = sizeof(double) * (size_t)(B * g * g);
-        const size_t bl = sizeof(double) * (size_t)(B * g), bo = sizeof(int32_t) * (size_t)(B * g);
-        const size_t bn = sizeof(double) * (size_t)B;
-        auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
-        const size_t bytes = al(bz) + 2 * al(bg) + al(bl) + al(bo) + al(bn);
-        void* ws = nullptr;
-        static bool pool_kept = false;   // keep freed workspace in the device's default pool across calls
-        if (!pool_kept) {
-            int dev = 0;
-            cudaMemPool_t pool;
-            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t keep = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            }
-            pool_kept = true;
-        }
-        cudaError_t e = cudaMallocAsync(&ws, bytes, cs);
-        if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd workspace (cudaMallocAsync)");
-        char* p = static_cast<char*>(ws);
+    int64_t off[6];
+    const int64_t need = (order >= 2 && gmax <= 32) ? ttsvd_ws_layout(batch, total, g, off) : 0;
+    if (need > 0 && workspace_dev && workspace_bytes >= need && !std::getenv("TTC_TTSVD_FUSED")) {
+        // warp-per-eigenproblem pipeline over the caller's workspace
+        char* p = static_cast<char*>(workspace_dev);
         ttc::TtsvdWs w;
-        w.z = reinterpret_cast<float*>(p); p += al(bz);
-        w.g = reinterpret_cast<double*>(p); p += al(bg);
-        w.v = reinterpret_cast<double*>(p); p += al(bg);
-        w.lam = reinterpret_cast<double*>(p); p += al(bl);
-        w.ord = reinterpret_cast<int32_t*>(p); p += al(bo);
-        w.nrm = reinterpret_cast<double*>(p);
-        e = ttc::launch_ttsvd_pipeline(a, w, cs);
-        const cudaError_t ef = cudaFreeAsync(ws, cs);
+        w.z = reinterpret_cast<float*>(p + off[0]);
+        w.g = reinterpret_cast<double*>(p + off[1]);
+        w.v = reinterpret_cast<double*>(p + off[2]);
+        w.lam = reinterpret_cast<double*>(p + off[3]);
+        w.ord = reinterpret_cast<int32_t*>(p + off[4]);
+        w.nrm = reinterpret_cast<double*>(p + off[5]);
+        const cudaError_t e = ttc::launch_ttsvd_pipeline(a, w, cs);
         if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd launch");
-        if (ef != cudaSuccess) return cuda_fail(ef, "ttc_tt_svd workspace free");
         return TTC_OK;
     }
     const size_t smem = sizeof(double) * (size_t)(2 * g * g + g + 2 * (g / 2 + 1) + 32) +

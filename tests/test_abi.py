@@ -28,7 +28,7 @@ def _declared_symbols():
 
 def test_library_exports_every_declared_symbol():
     syms = _declared_symbols()
-    assert len(syms) == 15
+    assert len(syms) == 16
     lib = ctypes.CDLL(ttc.LIB_PATH)
     for s in syms:
         assert hasattr(lib, s), s
@@ -272,3 +272,20 @@ def test_partition_uniform_and_errors():
         ttc.ttc_partition(np.ones(4), 0)
     with pytest.raises(ttc.TTCError):
         ttc.ttc_partition(np.array([1.0, -1.0]), 2)
+
+
+def test_tt_svd_workspace_sizes():
+    """Host-only sizing of ttc_tt_svd's caller-owned workspace: Z_n (B x prod(dims) floats), the Gram matrix and
+    its eigenvectors (B x g^2 doubles each), eigenvalues (B x g doubles), order (B x g int32), norms (B doubles),
+    each 256-byte aligned, g = the largest unfolding side; 0 where the fused launch runs (N = 1, or g > 32)."""
+    al = lambda v: (v + 255) // 256 * 256
+    B, dims = 7, (20, 20, 20)
+    g = 20
+    want = al(4 * B * 8000) + 2 * al(8 * B * g * g) + al(8 * B * g) + al(4 * B * g) + al(8 * B)
+    assert ttc.ttc_tt_svd_workspace(B, dims) == want
+    assert ttc.ttc_tt_svd_workspace(0, dims) == 0 or ttc.ttc_tt_svd_workspace(0, dims) >= 0
+    assert ttc.ttc_tt_svd_workspace(B, (5,)) == 0            # N = 1: no SVD step
+    assert ttc.ttc_tt_svd_workspace(B, (40, 40)) == 0        # side 40 > 32: fused launch
+    assert ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(2, 1)) > 0
+    with pytest.raises(ttc.TTCError):
+        ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(1, 1))
