@@ -66,6 +66,15 @@ __device__ __forceinline__ void stage(float* dst, const float* src, int n) {
     }
 }
 
+// Per-tile row state and per-column-tile column state of the store functors below.
+struct RowSt {
+    int m0, a, b;
+};
+struct ColSt {
+    float* p;
+    int a;   // < 0: column past N (nothing stored)
+};
+
 // Thread grid of one GEMM: txn = lx wx threads along m (4 rows each), tyn = (32 / lx) (8 / wx) along n (tm
 // columns each, 4 or 5); a warp covers lx x (32 / lx) of it, so its At loads touch lx distinct 16-byte quads and
 // its B loads 32 / lx distinct columns.  Chosen per product shape by a cost model: tiles x max(FFMA2 time,
@@ -82,8 +91,9 @@ __device__ __forceinline__ void score_grid(int M, int N, unsigned* best) {
     const Grid g = grid_of(c);
     const int ly = 32 / g.lx, txn = g.lx * g.wx, tyn = ly * (8 / g.wx), tm = g.tm;
     const int tiles = ((M + 4 * txn - 1) / (4 * txn)) * ((N + tyn * tm - 1) / (tyn * tm));
-    // per-k cost in quarter units: FFMA2 4 tm; wavefronts 4 max(1, lx/8) + tm max(1, ly/8)
-    const int wf = 4 * max(1, g.lx / 8) + tm * max(1, ly / 8);
+    // per-k cost in quarter units: FFMA2 4 tm; shared-memory wavefronts: the At load 2 (8 units), the B loads 2
+    // each (4 when all 32 lanes read distinct columns, lx = 1), tm / 4 of them
+    const int wf = 8 + (ly == 32 ? 4 : 2) * tm;
     atomicMin(best, ((unsigned)min(tiles * max(4 * tm, wf), 0xffffff) << 8) | (unsigned)c);
 }
 
@@ -97,17 +107,32 @@ __device__ __forceinline__ void tile_gemm(const Grid g, const float* At, int lda
                                           int N, int K, const Store& st) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, ly = 32 / g.lx;
     const int txn = g.lx * g.wx, tyn = ly * (8 / g.wx);
-    const int tx = (warp % g.wx) * g.lx + (lane & (g.lx - 1)), ty = (warp / g.wx) * ly + lane / g.lx;
+    // within the warp, tx from lane bits 1.. and ty from bit 0 and the bits above tx: each half-warp's At and B
+    // addresses then come in adjacent-lane runs or alternate lane by lane, which LDS.128 serves in one wavefront
+    // per half-warp (tools/lds_bench.cu; tx = lane & (lx - 1) would cost two for lx >= 4)
+    int ltx = 0, lty = lane;
+    if (g.lx > 1) {
+        ltx = (lane >> 1) & (g.lx - 1);
+        lty = (lane & 1) | ((lane >> (1 + __ffs(g.lx) - 1)) << 1);
+    }
+    const int tx = (warp % g.wx) * g.lx + ltx, ty = (warp / g.wx) * ly + lty;
     const bool vecA = (lda & 3) == 0, vecB = ((ldb | K) & 3) == 0;
     const uint32_t A0 = sa(At), B0 = sa(B);
     const int la = 4 * lda;   // bytes per q row of At
-    for (int mt = 0; mt < M; mt += 4 * txn)
-        for (int nt = 0; nt < N; nt += tyn * TM) {
+    // column tiles outer: the B addresses and the column halves of the output addresses are set once per column
+    // tile and reused down all its row tiles
+    for (int nt = 0; nt < N; nt += tyn * TM) {
+        uint32_t bp[TM];
+        ColSt cs[TM];
+#pragma unroll
+        for (int b2 = 0; b2 < TM; ++b2) {
+            const int n = nt + ty + tyn * b2;
+            bp[b2] = B0 + 4u * (uint32_t)(min(n, N - 1) * ldb);
+            cs[b2] = n < N ? st.col(n) : ColSt{nullptr, -1};
+        }
+        for (int mt = 0; mt < M; mt += 4 * txn) {
             const int m0 = mt + 4 * tx;
             uint32_t ap = A0 + 4u * m0;
-            uint32_t bp[TM];
-#pragma unroll
-            for (int b2 = 0; b2 < TM; ++b2) bp[b2] = B0 + 4u * (uint32_t)(min(nt + ty + tyn * b2, N - 1) * ldb);
             unsigned long long acc[2][TM];
 #pragma unroll
             for (int b2 = 0; b2 < TM; ++b2) acc[0][b2] = acc[1][b2] = 0ull;
@@ -145,12 +170,12 @@ __device__ __forceinline__ void tile_gemm(const Grid g, const float* At, int lda
             const auto rs = st.row(m0);
 #pragma unroll
             for (int b2 = 0; b2 < TM; ++b2) {
-                const int n = nt + ty + tyn * b2;
-                if (n >= N) continue;
+                if (cs[b2].a < 0) continue;
                 const float2 lo = up(acc[0][b2]), hi = up(acc[1][b2]);
-                st(rs, n, make_float4(lo.x, lo.y, hi.x, hi.y));
+                st(rs, cs[b2], make_float4(lo.x, lo.y, hi.x, hi.y));
             }
         }
+    }
 }
 template <class Store>
 __device__ __forceinline__ void gemm(const Grid g, const float* At, int lda, const float* B, int ldb, int M, int N,
@@ -159,30 +184,30 @@ __device__ __forceinline__ void gemm(const Grid g, const float* At, int lda, con
     else tile_gemm<4>(g, At, lda, B, ldb, M, N, K, st);
 }
 
-// Stores of the three GEMM kinds (row state from row(m0), computed once per tile).  Rows m0 + u >= M dropped.
-struct RowSt {
-    int m0, a, b;
-};
+// Stores of the three GEMM kinds: row(m0) once per tile, col(n) once per column tile, then (row, col, v) for
+// the thread's 4 results (rows m0..m0+3) of column n.  Rows m0 + u >= M are dropped.
 struct StoreLeft {   // P'^T[s][row] (row stride ld), m = pr, n = i + I s; row = pr + prow i, or i + I pr (rev)
     float* out;
     int ld, prow, I, M;
     bool rev;
     __device__ __forceinline__ RowSt row(int m0) const { return RowSt{m0, m0 + 3 < M ? 4 : M - m0, 0}; }
-    __device__ __forceinline__ void operator()(const RowSt& rs, int n, float4 v) const {
+    __device__ __forceinline__ ColSt col(int n) const {
         const int s = n / I, i = n - s * I;
+        return ColSt{out + (size_t)s * ld + (rev ? i : prow * i), 0};
+    }
+    __device__ __forceinline__ void operator()(const RowSt& rs, const ColSt& c, float4 v) const {
+        const float w[4] = {v.x, v.y, v.z, v.w};
         if (rev) {   // the new mode fastest: the 4 rows are I apart
-            float* o = out + (size_t)s * ld + i + I * rs.m0;
-            const float w[4] = {v.x, v.y, v.z, v.w};
+            float* o = c.p + I * rs.m0;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (u < rs.a) o[I * u] = w[u];
             return;
         }
-        float* o = out + (size_t)s * ld + prow * i + rs.m0;
+        float* o = c.p + rs.m0;
         if (rs.a == 4 && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
             *reinterpret_cast<float4*>(o) = v;
         } else {
-            const float w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (u < rs.a) o[u] = w[u];
@@ -196,10 +221,11 @@ struct StoreRight {  // Q'[i + I pc][r] (row stride R), m = r + R i, n = pc
         const int i0 = m0 / R;
         return RowSt{m0, i0, m0 - i0 * R};
     }
-    __device__ __forceinline__ void operator()(const RowSt& rs, int n, float4 v) const {
+    __device__ __forceinline__ ColSt col(int n) const { return ColSt{out + (size_t)I * n * R, 0}; }
+    __device__ __forceinline__ void operator()(const RowSt& rs, const ColSt& c, float4 v) const {
         const float w[4] = {v.x, v.y, v.z, v.w};
         if (rs.b + 3 < R) {   // the 4 rows lie in one row of Q' (M = R I, so m0 + 3 < M as well)
-            float* o = out + ((size_t)rs.a + (size_t)I * n) * R + rs.b;
+            float* o = c.p + (size_t)rs.a * R + rs.b;
             if ((reinterpret_cast<uintptr_t>(o) & 15u) == 0) { *reinterpret_cast<float4*>(o) = v; return; }
 #pragma unroll
             for (int u = 0; u < 4; ++u) o[u] = w[u];
@@ -210,7 +236,7 @@ struct StoreRight {  // Q'[i + I pc][r] (row stride R), m = r + R i, n = pc
             const int m = rs.m0 + u;
             if (m >= M) break;
             const int i = m / R, r = m - i * R;
-            out[((size_t)i + (size_t)I * n) * R + r] = w[u];
+            c.p[(size_t)i * R + r] = w[u];
         }
     }
 };
@@ -224,17 +250,17 @@ struct StoreD {      // out[offr[row] + offc[col]], m = row, n = col (streaming 
         const bool v4 = m0 + 3 < M && offr[m0 + 1] == o0 + 1 && offr[m0 + 2] == o0 + 2 && offr[m0 + 3] == o0 + 3;
         return RowSt{m0, o0, v4 ? 1 : 0};
     }
-    __device__ __forceinline__ void operator()(const RowSt& rs, int n, float4 v) const {
-        float* o = out + offc[n] + rs.a;
+    __device__ __forceinline__ ColSt col(int n) const { return ColSt{out + offc[n], 0}; }
+    __device__ __forceinline__ void operator()(const RowSt& rs, const ColSt& c, float4 v) const {
+        float* o = c.p + rs.a;
         if (rs.b && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
             __stcs(reinterpret_cast<float4*>(o), v);
             return;
         }
         const float w[4] = {v.x, v.y, v.z, v.w};
-        float* oc = out + offc[n];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (rs.m0 + u < M) __stcs(oc + offr[rs.m0 + u], w[u]);
+            if (rs.m0 + u < M) __stcs(c.p + offr[rs.m0 + u], w[u]);
     }
 };
 

@@ -25,7 +25,11 @@ __global__ void lds_kernel(float* out, int iters) {
         case 10: idx = lane & 1; break;            // 2 distinct, alternating
         case 11: idx = lane >> 1; break;           // 16 distinct, pairs share
         case 12: idx = (lane & 3) + 4 * (lane >> 4); break;  // 8 distinct: 4 strided per half
-        default: idx = (lane >> 2) & 3; break;     // 4 distinct, 4 consecutive share, halves identical
+        case 13: idx = (lane >> 2) & 3; break;     // 4 distinct, 4 consecutive share, halves identical
+        case 14: idx = (lane & 1) | ((lane >> 3) << 1); break;   // 8 distinct: alternating pairs per quarter
+        case 15: idx = (lane >> 1) & 3; break;     // 4 distinct, pairs share, quarters identical
+        case 16: idx = 2 * lane; break;            // 32 distinct, 32-byte stride
+        default: idx = (lane & 1) | ((lane >> 2) << 1); break;   // 16 distinct: alternating, quad steps
     }
     float acc = 0.f;
     const float* p = s + 4 * idx;
@@ -49,7 +53,7 @@ int main() {
     cudaMalloc(&out, 148 * 256 * sizeof(float));
 #define RUN(P, V) lds_kernel<P, V><<<148, 256>>>(out, 1000);
     RUN(0, 4) RUN(1, 4) RUN(2, 4) RUN(3, 4) RUN(4, 4) RUN(5, 4) RUN(6, 4) RUN(7, 4)
-    RUN(8, 4) RUN(9, 4) RUN(10, 4) RUN(11, 4) RUN(12, 4) RUN(13, 4)
+    RUN(8, 4) RUN(9, 4) RUN(10, 4) RUN(11, 4) RUN(12, 4) RUN(13, 4) RUN(14, 4) RUN(15, 4) RUN(16, 4) RUN(17, 4)
     RUN(0, 2) RUN(1, 2) RUN(2, 2) RUN(3, 2) RUN(4, 2) RUN(5, 2) RUN(6, 2) RUN(7, 2)
     cudaDeviceSynchronize();
     printf("done %s\n", cudaGetErrorString(cudaGetLastError()));
