@@ -487,7 +487,9 @@ __device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* 
             // next round: players 1..np-1 advance one position (np - 1 wraps to 1); player 0 stays
             if (px != 0) px = px == np - 1 ? 1 : px + 1;
             py = py == np - 1 ? 1 : py + 1;
-            any |= __any_sync(0xffffffffu, rot);
+            const bool round_rot = __any_sync(0xffffffffu, rot);
+            any |= round_rot;
+            if (!round_rot) continue;   // nothing to rotate this round: G and V stay (no buffer swap)
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < 5; ++u) {   // upper-triangle blocks q1 <= q2 (G symmetric: the mirror is the transpose)
