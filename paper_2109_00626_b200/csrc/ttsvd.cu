@@ -372,6 +372,52 @@ __device__ void gram_tiled(const float* Z, int m, int ncols, double* gs, double*
     }
 }
 
+// Z[dst(e)] = src[e] for the tensor's elements e = tid, tid + blockDim, ... read contiguously; dst by the
+// mixed-radix walk of e (radices rad, X^rho strides dstr, source mode order) advanced by blockDim's digits with
+// carries (NW >= N digits in registers; NW = 0: per-element division).  Returns this thread's sum of squares.
+template <int NW>
+__device__ __forceinline__ double scatter_walk(const TtsvdArgs& a, const float* src, float* Z, const int32_t* rad_s,
+                                               const int32_t* dstr_s) {
+    const int N = a.N;
+    double nrm = 0.0;
+    if (NW == 0) {
+        for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
+            int q = e, off = 0;
+            for (int p = 0; p < N; ++p) { off += (q % rad_s[p]) * dstr_s[p]; q /= rad_s[p]; }
+            const float v = __ldg(src + e);
+            Z[off] = v;
+            nrm += (double)v * v;
+        }
+        return nrm;
+    }
+    constexpr int W = NW > 0 ? NW : 1;
+    int dig[W], sd[W], rad[W], dstr[W];
+    int off = 0, q = threadIdx.x, r = blockDim.x;
+#pragma unroll
+    for (int p = 0; p < W; ++p) {
+        rad[p] = p < N ? rad_s[p] : 1;
+        dstr[p] = p < N ? dstr_s[p] : 0;
+        dig[p] = q % rad[p]; q /= rad[p];
+        sd[p] = r % rad[p]; r /= rad[p];
+        off += dig[p] * dstr[p];
+    }
+    for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
+        const float v = __ldg(src + e);
+        Z[off] = v;
+        nrm += (double)v * v;
+        int carry = 0;
+#pragma unroll
+        for (int p = 0; p < W; ++p) {   // (padding digits: radix 1, stride 0 -> no effect)
+            int d = dig[p] + sd[p] + carry;
+            carry = d >= rad[p];
+            if (carry) d -= rad[p];
+            off += (d - dig[p]) * dstr[p];
+            dig[p] = d;
+        }
+    }
+    return nrm;
+}
+
 __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a, const TtsvdWs w) {
     extern __shared__ __align__(16) unsigned char sraw[];
     __shared__ int32_t rad[TTC_MAX_ORDER];
@@ -399,40 +445,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a
         for (int p = 0; p < N; ++p) { const int k = -1 - rad[p]; rad[p] = a.dims[k]; dstr[p] = (int32_t)xs[k]; }
     }
     __syncthreads();
-    double nrm = 0.0;
-    {
-        int dig[kWalkMax], sd[kWalkMax];
-        int off = 0;   // (elems <= 16384)
-        const bool fast = N <= kWalkMax;
-        if (fast) {
-            int q = threadIdx.x, r = blockDim.x;
-#pragma unroll
-            for (int p = 0; p < kWalkMax; ++p)
-                if (p < N) { dig[p] = q % rad[p]; q /= rad[p]; sd[p] = r % rad[p]; r /= rad[p]; off += dig[p] * dstr[p]; }
-        }
-        for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
-            if (!fast) {
-                int q = e;
-                off = 0;
-                for (int p = 0; p < N; ++p) { off += (q % rad[p]) * dstr[p]; q /= rad[p]; }
-            }
-            const float v = __ldg(src + e);
-            Z[off] = v;
-            nrm += (double)v * v;
-            if (fast) {
-                int carry = 0;
-#pragma unroll
-                for (int p = 0; p < kWalkMax; ++p)
-                    if (p < N) {
-                        int d = dig[p] + sd[p] + carry;
-                        carry = d >= rad[p];
-                        if (carry) d -= rad[p];
-                        off += (d - dig[p]) * dstr[p];
-                        dig[p] = d;
-                    }
-            }
-        }
-    }
+    double nrm = N <= 4 ? scatter_walk<4>(a, src, Z, rad, dstr) : scatter_walk<0>(a, src, Z, rad, dstr);
     nrm = block_sum(nrm, red);   // (its barriers also publish Z)
     for (int e = threadIdx.x; e < a.elems; e += blockDim.x) zg[e] = Z[e];
     if (threadIdx.x == 0) {
