@@ -322,24 +322,19 @@ __device__ void gram_to(const float* Z, int m, int ncols, double* g) {
     }
 }
 
-// The same Gram matrix as register-tiled fp64 products: 4 x 4 tiles of the upper triangle, the summed index
-// split into chunks so that every thread has a (tile, chunk) item; partial tiles added into gs (shared, side^2
-// doubles) with shared-memory atomics, then gs (mirrored) written to g.  Element (i, t) of the side x len
-// operand is Z[i si + t st].
-__device__ void gram_tiled(const float* Z, int m, int ncols, double* gs, double* g) {
+// The same Gram matrix as register-tiled fp64 products: 4 x 4 tiles of the upper triangle, one warp per tile,
+// its lanes splitting the summed index (lane, lane + 32, ...), the 16 partial sums reduced by warp shuffles (no
+// atomics), then written to g and mirrored.  Element (i, t) of the side x len operand is Z[i si + t st].
+__device__ void gram_tiled(const float* Z, int m, int ncols, double* g) {
     const bool rows_side = m <= ncols;
     const int side = rows_side ? m : ncols, len = rows_side ? ncols : m;
     const int si = rows_side ? 1 : m, st = rows_side ? m : 1;
     const int T = (side + 3) >> 2, pairs = T * (T + 1) / 2;
-    const int chunks = max(1, min(len, (int)blockDim.x / pairs)), clen = (len + chunks - 1) / chunks;
-    for (int e = threadIdx.x; e < side * side; e += blockDim.x) gs[e] = 0.0;
-    __syncthreads();
-    for (int it = threadIdx.x; it < pairs * chunks; it += blockDim.x) {
-        const int ch = it / pairs;
-        int p = it - ch * pairs, ti = 0;
+    const int wp = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int it = wp; it < pairs; it += nw) {
+        int p = it, ti = 0;
         while (p >= T - ti) { p -= T - ti; ++ti; }   // upper-triangle tile (ti, tj), tj >= ti
         const int tj = ti + p, i0 = 4 * ti, j0 = 4 * tj;
-        const int t0 = ch * clen, t1 = min(len, t0 + clen);
         double acc[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -348,7 +343,7 @@ __device__ void gram_tiled(const float* Z, int m, int ncols, double* gs, double*
         int ia[4], ja[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) { ia[u] = min(i0 + u, side - 1) * si; ja[u] = min(j0 + u, side - 1) * si; }
-        for (int t = t0; t < t1; ++t) {
+        for (int t = l; t < len; t += 32) {
             const float* zt = Z + t * st;
             double x[4], y[4];
 #pragma unroll
@@ -362,13 +357,17 @@ __device__ void gram_tiled(const float* Z, int m, int ncols, double* gs, double*
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v)
-                if (i0 + u < side && j0 + v < side) atomicAdd(&gs[(i0 + u) * side + j0 + v], acc[u][v]);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < side * side; e += blockDim.x) {
-        const int i = e / side, j = e - i * side;
-        // tiles cover (i, j) with tile(i) <= tile(j); the rest mirror
-        g[e] = (i >> 2) <= (j >> 2) ? gs[e] : gs[j * side + i];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[u][v] += __shfl_xor_sync(0xffffffffu, acc[u][v], o);
+        if (l == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int i = i0 + u, j = j0 + v;
+                    if (i < side && j < side) { g[i * side + j] = acc[u][v]; g[j * side + i] = acc[u][v]; }
+                }
+        }
     }
 }
 
@@ -418,7 +417,7 @@ __device__ __forceinline__ double scatter_walk(const TtsvdArgs& a, const float* 
     return nrm;
 }
 
-__global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a, const TtsvdWs w) {
+__global__ void __launch_bounds__(kThreads, 4) ttsvd_first_kernel(const TtsvdArgs a, const TtsvdWs w) {
     extern __shared__ __align__(16) unsigned char sraw[];
     __shared__ int32_t rad[TTC_MAX_ORDER];
     __shared__ int32_t dstr[TTC_MAX_ORDER];
@@ -430,9 +429,6 @@ __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a
     // the source's modes in memory order (X^rho's modes sorted by source stride), with X^rho's compact strides:
     // the source is read contiguously (coalesced) and scattered into Z in X^rho order
     if (threadIdx.x == 0) {
-        int64_t cs = 1;
-        int64_t xs[TTC_MAX_ORDER];
-        for (int k = 0; k < N; ++k) { xs[k] = cs; cs *= a.dims[k]; }
         for (int p = 0; p < N; ++p) {
             int best = -1;
             for (int k = 0; k < N; ++k) {
@@ -442,7 +438,13 @@ __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a
             }
             rad[p] = -1 - best;
         }
-        for (int p = 0; p < N; ++p) { const int k = -1 - rad[p]; rad[p] = a.dims[k]; dstr[p] = (int32_t)xs[k]; }
+        for (int p = 0; p < N; ++p) {
+            const int k = -1 - rad[p];
+            int32_t xs = 1;   // X^rho's compact stride of mode k
+            for (int k2 = 0; k2 < k; ++k2) xs *= a.dims[k2];
+            rad[p] = a.dims[k];
+            dstr[p] = xs;
+        }
     }
     __syncthreads();
     double nrm = N <= 4 ? scatter_walk<4>(a, src, Z, rad, dstr) : scatter_walk<0>(a, src, Z, rad, dstr);
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_first_kernel(const TtsvdArgs a
         w.nrm[b] = nrm;
         a.ranks[(int64_t)b * (N + 1)] = 1;
     }
-    gram_tiled(Z, a.dims[0], a.elems / a.dims[0], red + 32 + ((a.elems + 1) >> 1), w.g + (int64_t)b * a.gmax * a.gmax);
+    gram_tiled(Z, a.dims[0], a.elems / a.dims[0], w.g + (int64_t)b * a.gmax * a.gmax);
 }
 
 // Cyclic Jacobi of G (n x n, n <= 32) by one warp.  Same round-robin pairs and rotation rule as jacobi(); each
@@ -715,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 3) ttsvd_step_kernel(const TtsvdArgs
     float* zo = w.z + (int64_t)b * a.elems;
     for (int e = threadIdx.x; e < nel; e += blockDim.x) zo[e] = U[e];
     const int m2 = R * a.dims[n + 1];
-    gram_tiled(U, m2, nel / m2, V, w.g + (int64_t)b * gm * gm);   // (V is free by now)
+    gram_tiled(U, m2, nel / m2, w.g + (int64_t)b * gm * gm);
 }
 
 }  // namespace
@@ -729,7 +731,7 @@ cudaError_t launch_ttsvd(const TtsvdArgs& a, size_t smem_bytes, cudaStream_t s) 
 
 cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStream_t s) {
     const int gm = a.gmax;
-    const size_t smem_first = sizeof(double) * (32 + (size_t)gm * gm) + sizeof(double) * (size_t)((a.elems + 1) / 2);
+    const size_t smem_first = sizeof(double) * 32 + sizeof(double) * (size_t)((a.elems + 1) / 2);
     const size_t smem_jac = (sizeof(double) * (size_t)(3 * gm * gm + 2 * 16 + 32) + sizeof(int) * 96) * kJacWarps;
     const size_t smem_step = sizeof(double) * (size_t)(gm * gm + gm) + sizeof(int) * (size_t)((gm + 3) & ~3) +
                              2 * sizeof(int64_t) + 2 * sizeof(float) * (size_t)a.elems;
@@ -737,6 +739,10 @@ cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStre
     if ((e = cudaFuncSetAttribute(ttsvd_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_first)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(ttsvd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_jac)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(ttsvd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_step)) != cudaSuccess) return e;
+    // shared memory bounds how many tensors an SM holds at once: ask for the largest carveout
+    if ((e = cudaFuncSetAttribute(ttsvd_first_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(ttsvd_jacobi_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(ttsvd_step_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
     ttsvd_first_kernel<<<a.B, kThreads, smem_first, s>>>(a, w);
     for (int n = 0; n + 1 < a.N; ++n) {
         ttsvd_jacobi_kernel<<<(a.B + kJacWarps - 1) / kJacWarps, 32 * kJacWarps, smem_jac, s>>>(a, w, n);
