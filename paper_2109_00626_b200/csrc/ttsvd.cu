@@ -635,13 +635,36 @@ __global__ void __launch_bounds__(kThreads, 3) ttsvd_step_kernel(const TtsvdArgs
             const int j = e / m, i = e - j * m;
             U[e] = (float)V[i * side + ord[j]];
         }
-    } else {
-        for (int e = threadIdx.x; e < m * R; e += blockDim.x) {
-            const int j = e / m, r = e - j * m;
-            const int col = ord[j];
-            double acc = 0.0;
-            for (int c = 0; c < ncols; ++c) acc += (double)Z[r + m * c] * V[c * side + col];
-            U[e] = lam[col] > 0.0 ? (float)(acc / sqrt(lam[col])) : 0.f;
+    } else {           // U = Z V_R S_R^-1 in 4 (r) x 4 (j) register tiles, fp64 accumulation
+        const int tr = (m + 3) >> 2, tj = (R + 3) >> 2;
+        for (int it = threadIdx.x; it < tr * tj; it += blockDim.x) {
+            const int r0 = 4 * (it % tr), j0 = 4 * (it / tr);
+            int col[4], rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { col[u] = ord[min(j0 + u, R - 1)]; rr[u] = min(r0 + u, m - 1); }
+            double acc[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+            for (int c = 0; c < ncols; ++c) {
+                double x[4], y[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { x[u] = Z[rr[u] + m * c]; y[u] = V[c * side + col[u]]; }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = fma(x[u], y[v], acc[u][v]);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                if (j0 + v >= R) break;
+                const double l = lam[col[v]];
+                const double inv = l > 0.0 ? 1.0 / sqrt(l) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (r0 + u < m) U[r0 + u + m * (j0 + v)] = l > 0.0 ? (float)(acc[u][v] * inv) : 0.f;
+            }
         }
     }
     __syncthreads();
