@@ -489,10 +489,13 @@ __device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* 
                 double c = 1.0, s = 0.0;
                 if (y < n) {
                     const double app = G[x * n + x], aqq = G[y * n + y], apq = G[x * n + y];
-                    if (fabs(apq) > 1e-300 && fabs(apq) > DBL_EPSILON * sqrt(fabs(app * aqq))) {
-                        const double th = (aqq - app) / (2.0 * apq);
-                        const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-                        c = 1.0 / sqrt(tt * tt + 1.0);
+                    // the same rule and rotation as jacobi() with a shorter dependent chain (one sqrt, one divide,
+                    // one rsqrt): t = sign(d) 2 a_pq / (|d| + sqrt(d^2 + 4 a_pq^2)), d = a_qq - a_pp (= sign(th) /
+                    // (|th| + sqrt(th^2 + 1)) with th = d / (2 a_pq)), c = 1 / sqrt(1 + t^2), s = t c
+                    if (fabs(apq) > 1e-300 && apq * apq > DBL_EPSILON * DBL_EPSILON * fabs(app * aqq)) {
+                        const double d = aqq - app, b2 = apq + apq;
+                        const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
+                        c = rsqrt(fma(tt, tt, 1.0));
                         s = tt * c;
                         rot = true;
                     }
