@@ -281,7 +281,8 @@ __global__ void __launch_bounds__(kThreads) ttsvd_kernel(const TtsvdArgs a) {
 // are separate CTA-per-tensor kernels, passing Z_n, the Gram matrix and its eigenvectors through a
 // workspace (L2-resident at A2's sizes).
 //   first  : Z_0 <- X^rho, ||X||^2, Gram of Z_0
-//   jacobi : (per step n) eigenvectors, eigenvalues in descending order, the delta-truncated rank R_n
+//   jacobi : (per step n) eigenvectors (two warps per eigenproblem: G and V updates overlapped), eigenvalues
+//            in descending order, the delta-truncated rank R_n
 //   step   : (per step n) core n = U (R24 signs), Z_{n+1}, its Gram (or, after the last step, core N)
 
 // Gram matrix of Z (m x ncols, Z[r + m c]) of the smaller side, fp64, into g (side x side, row-major).
@@ -457,17 +458,29 @@ __global__ void __launch_bounds__(kThreads, 4) ttsvd_first_kernel(const TtsvdArg
     gram_tiled(Z, a.dims[0], a.elems / a.dims[0], w.g + (int64_t)b * a.gmax * a.gmax);
 }
 
-// Cyclic Jacobi of G (n x n, n <= 32) by one warp.  Same round-robin pairs and rotation rule as jacobi(); each
-// round applies all its rotations at once as 2 x 2 block updates G' = J_p^T G J_q (G double-buffered, so one
-// pass and no ordering between blocks) and V' = V J.  Returns the buffer holding the final G.
-__device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* cs, double* sn, int* pa, int* pb) {
+// Cyclic Jacobi of G (n x n, n <= 32) on a PAIR of warps, with no CTA barriers: same round-robin pairs and
+// rotation rule as jacobi() (one sqrt, one divide, one rsqrt per rotation); every round applies its rotations at
+// once as 2 x 2 upper-triangle block updates G' = J_p^T G J_q mirrored (G double-buffered, so one pass), rounds
+// that rotate nothing are skipped, and the iteration stops after a sweep that rotates no pair.
+// The G warp (role 0) computes each round's rotations into one of
+// two parameter buffers and applies the two-sided block update to G; the V warp (role 1) applies the previous
+// round's rotations to V (V J) meanwhile, so the V update leaves the critical path.  The two warps meet once a
+// round at a 64-thread named barrier `bar`; ctl[0] publishes "round r rotates" and ctl[1] "stop".  Returns the
+// buffer holding the final G (in the G warp).
+struct JacParams {
+    double cs[2][16], sn[2][16];
+    int pa[2][16], pb[2][16];
+    int ctl[4];
+};
+__device__ __forceinline__ void pair_bar(int bar) { asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory"); }
+
+__device__ double* jacobi_pair(double* G, double* Gn, double* V, int n, JacParams& P, int role, int bar) {
     const int lane = threadIdx.x & 31;
-    for (int e = lane; e < n * n; e += 32) V[e] = (e / n == e % n) ? 1.0 : 0.0;
     const int np = (n + 1) & ~1, half = np / 2;
-    // index walks without divisions: e += 32 over (q1, q2) = (e / half, e % half) and (k, q) = (e / half, ...)
     const int d1 = 32 / half, d2 = 32 - d1 * half;
     const int k0 = lane / half, q0 = lane - k0 * half;
-    // this lane's upper-triangle blocks e = lane + 32 u < half (half + 1) / 2 (<= 5 for half <= 16): q1 << 8 | q2
+    if (role == 1)
+        for (int e = lane; e < n * n; e += 32) V[e] = (e / n == e % n) ? 1.0 : 0.0;
     int bp[5];
 #pragma unroll
     for (int u = 0; u < 5; ++u) {
@@ -476,103 +489,121 @@ __device__ double* jacobi_warp(double* G, double* Gn, double* V, int n, double* 
         while (p >= half - q1) { p -= half - q1; ++q1; }
         bp[u] = (q1 << 8) | (q1 + p);
     }
-    __syncwarp();
-    for (int sweep = 0; sweep < kSweeps; ++sweep) {
-        bool any = false;
-        // round-robin positions of this lane's two players (lane < half): players 1..np-1 rotate by one a round
-        int px = lane == 0 ? 0 : lane, py = np - 1 - lane;   // pos(j) at t = 0 is j
-        for (int t = 0; t < np - 1; ++t) {
+    int px = lane == 0 ? 0 : lane, py = np - 1 - lane;   // this lane's players' positions (pos(j) at t = 0 is j)
+    int sweep = 0, t = 0, r = 0;
+    bool any = false;
+    for (;; ++r) {
+        const int cur = r & 1;
+        if (role == 0) {
+            // stop after a sweep that rotated nothing (or kSweeps sweeps): decided at the start of a sweep
+            bool stop = false;
+            if (t == 0 && r > 0) {
+                stop = !any || sweep == kSweeps;
+                any = false;
+            }
             bool rot = false;
-            if (lane < half) {
+            if (!stop && lane < half) {
                 int x = px, y = py;
                 if (x > y) { const int u = x; x = y; y = u; }
-                double c = 1.0, s = 0.0;
+                double c = 1.0, sv = 0.0;
                 if (y < n) {
                     const double app = G[x * n + x], aqq = G[y * n + y], apq = G[x * n + y];
-                    // the same rule and rotation as jacobi() with a shorter dependent chain (one sqrt, one divide,
-                    // one rsqrt): t = sign(d) 2 a_pq / (|d| + sqrt(d^2 + 4 a_pq^2)), d = a_qq - a_pp (= sign(th) /
-                    // (|th| + sqrt(th^2 + 1)) with th = d / (2 a_pq)), c = 1 / sqrt(1 + t^2), s = t c
                     if (fabs(apq) > 1e-300 && apq * apq > DBL_EPSILON * DBL_EPSILON * fabs(app * aqq)) {
                         const double d = aqq - app, b2 = apq + apq;
                         const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
                         c = rsqrt(fma(tt, tt, 1.0));
-                        s = tt * c;
+                        sv = tt * c;
                         rot = true;
                     }
                 }
-                cs[lane] = c; sn[lane] = s; pa[lane] = x; pb[lane] = y;
+                P.cs[cur][lane] = c; P.sn[cur][lane] = sv; P.pa[cur][lane] = x; P.pb[cur][lane] = y;
             }
-            // next round: players 1..np-1 advance one position (np - 1 wraps to 1); player 0 stays
+            const bool rr = __any_sync(0xffffffffu, rot);
+            any |= rr;
+            if (lane == 0) P.ctl[cur] = (rr ? 1 : 0) | (stop ? 2 : 0);   // parity slot: the V warp reads it after
+                                                                          // this barrier, before round r + 2 reuses it
             if (px != 0) px = px == np - 1 ? 1 : px + 1;
             py = py == np - 1 ? 1 : py + 1;
-            const bool round_rot = __any_sync(0xffffffffu, rot);
-            any |= round_rot;
-            if (!round_rot) continue;   // nothing to rotate this round: G and V stay (no buffer swap)
-            __syncwarp();
+            if (++t == np - 1) { t = 0; ++sweep; }
+            pair_bar(bar);   // round r's rotations published; the V warp has finished round r - 1
+            if (stop) break;
+            if (rr) {
 #pragma unroll
-            for (int u = 0; u < 5; ++u) {   // upper-triangle blocks q1 <= q2 (G symmetric: the mirror is the transpose)
-                if (bp[u] < 0) break;
-                const int q1 = bp[u] >> 8, q2 = bp[u] & 255;
-                const int a1 = pa[q1], b1 = pb[q1], a2 = pa[q2], b2 = pb[q2];
-                const double c1 = cs[q1], s1 = sn[q1], c2 = cs[q2], s2 = sn[q2];
-                const bool hb1 = b1 < n, hb2 = b2 < n;
-                const double g00 = G[a1 * n + a2], g01 = hb2 ? G[a1 * n + b2] : 0.0;
-                const double g10 = hb1 ? G[b1 * n + a2] : 0.0, g11 = hb1 && hb2 ? G[b1 * n + b2] : 0.0;
-                const double x00 = c2 * g00 - s2 * g01, x01 = s2 * g00 + c2 * g01;   // B J2
-                const double x10 = c2 * g10 - s2 * g11, x11 = s2 * g10 + c2 * g11;
-                const double y00 = c1 * x00 - s1 * x10, y01 = c1 * x01 - s1 * x11;   // J1^T (B J2)
-                const double y10 = s1 * x00 + c1 * x10, y11 = s1 * x01 + c1 * x11;
-                Gn[a1 * n + a2] = y00;
-                Gn[a2 * n + a1] = y00;
-                if (hb2) { Gn[a1 * n + b2] = y01; Gn[b2 * n + a1] = y01; }
-                if (hb1) { Gn[b1 * n + a2] = y10; Gn[a2 * n + b1] = y10; }
-                if (hb1 && hb2) { Gn[b1 * n + b2] = y11; Gn[b2 * n + b1] = y11; }
+                for (int u = 0; u < 5; ++u) {
+                    if (bp[u] < 0) break;
+                    const int q1 = bp[u] >> 8, q2 = bp[u] & 255;
+                    const int a1 = P.pa[cur][q1], b1 = P.pb[cur][q1], a2 = P.pa[cur][q2], b2 = P.pb[cur][q2];
+                    const double c1 = P.cs[cur][q1], s1 = P.sn[cur][q1], c2 = P.cs[cur][q2], s2 = P.sn[cur][q2];
+                    const bool hb1 = b1 < n, hb2 = b2 < n;
+                    const double g00 = G[a1 * n + a2], g01 = hb2 ? G[a1 * n + b2] : 0.0;
+                    const double g10 = hb1 ? G[b1 * n + a2] : 0.0, g11 = hb1 && hb2 ? G[b1 * n + b2] : 0.0;
+                    const double x00 = c2 * g00 - s2 * g01, x01 = s2 * g00 + c2 * g01;
+                    const double x10 = c2 * g10 - s2 * g11, x11 = s2 * g10 + c2 * g11;
+                    const double y00 = c1 * x00 - s1 * x10, y01 = c1 * x01 - s1 * x11;
+                    const double y10 = s1 * x00 + c1 * x10, y11 = s1 * x01 + c1 * x11;
+                    Gn[a1 * n + a2] = y00;
+                    Gn[a2 * n + a1] = y00;
+                    if (hb2) { Gn[a1 * n + b2] = y01; Gn[b2 * n + a1] = y01; }
+                    if (hb1) { Gn[b1 * n + a2] = y10; Gn[a2 * n + b1] = y10; }
+                    if (hb1 && hb2) { Gn[b1 * n + b2] = y11; Gn[b2 * n + b1] = y11; }
+                }
+                __syncwarp();
+                double* tmp = G; G = Gn; Gn = tmp;
             }
-            int k = k0, q = q0;
-            for (int e = lane; e < n * half; e += 32) {      // V J: row k, pair q
-                if (e != lane) { k += d1; q += d2; if (q >= half) { q -= half; ++k; } }
-                const int x = pa[q], y = pb[q];
-                if (y >= n || sn[q] == 0.0) continue;
-                const double c = cs[q], s = sn[q];
-                const double vx = V[k * n + x], vy = V[k * n + y];
-                V[k * n + x] = c * vx - s * vy;
-                V[k * n + y] = s * vx + c * vy;
+        } else {
+            pair_bar(bar);
+            const int f = P.ctl[cur];
+            if (f & 2) break;
+            if (f & 1) {
+                int k = k0, q = q0;
+                for (int e = lane; e < n * half; e += 32) {      // V J: row k, pair q
+                    if (e != lane) { k += d1; q += d2; if (q >= half) { q -= half; ++k; } }
+                    const int x = P.pa[cur][q], y = P.pb[cur][q];
+                    if (y >= n || P.sn[cur][q] == 0.0) continue;
+                    const double c = P.cs[cur][q], sv = P.sn[cur][q];
+                    const double vx = V[k * n + x], vy = V[k * n + y];
+                    V[k * n + x] = c * vx - sv * vy;
+                    V[k * n + y] = sv * vx + c * vy;
+                }
             }
-            __syncwarp();
-            double* tmp = G; G = Gn; Gn = tmp;
         }
-        if (!any) break;
     }
+    // both warps leave at the same barrier (the V warp's last update finished before it); the returned G is the
+    // G warp's final buffer (the V warp's copy of the pointer is not used)
     return G;
 }
 
-constexpr int kJacWarps = 4;
+constexpr int kJacPairs = 4;   // eigenproblems per CTA, two warps each
 
-__global__ void __launch_bounds__(32 * kJacWarps) ttsvd_jacobi_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
+__global__ void __launch_bounds__(64 * kJacPairs) ttsvd_jacobi_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
     extern __shared__ __align__(16) unsigned char sraw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.x * kJacWarps + warp;
-    if (b >= a.B) return;   // (warp-local from here on: no CTA barriers)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp >> 1, role = warp & 1;
+    const int b = blockIdx.x * kJacPairs + pair;
+    if (b >= a.B) return;   // (both warps of the pair leave: only pair-local barriers below)
     const int g2 = a.gmax * a.gmax, N = a.N;
-    double* G = reinterpret_cast<double*>(sraw) + (size_t)warp * (3 * g2 + 2 * 16 + 32);
+    double* G = reinterpret_cast<double*>(sraw) + (size_t)pair * (3 * g2 + 32);
     double* Gn = G + g2;
     double* V = Gn + g2;
-    double* cs = V + g2;
-    double* sn = cs + 16;
-    double* lam = sn + 16;                                   // 32
-    int* pa = reinterpret_cast<int*>(sraw + sizeof(double) * (size_t)kJacWarps * (3 * g2 + 2 * 16 + 32)) + warp * 96;
-    int* pb = pa + 16;
-    int* ord = pb + 16;                                      // 32
-    int* misc = ord + 32;                                    // [0]: R
+    double* lam = V + g2;                                    // 32
+    JacParams& P = reinterpret_cast<JacParams*>(sraw + sizeof(double) * (size_t)kJacPairs * (3 * g2 + 32))[pair];
+    __shared__ int ord_s[kJacPairs][32];
+    int* ord = ord_s[pair];
     int32_t* rk = a.ranks + (int64_t)b * (N + 1);
     const int Rprev = rk[n];
     int64_t cur = Rprev;
     for (int k = n; k < N; ++k) cur *= a.dims[k];
     const int m = Rprev * a.dims[n], ncols = (int)(cur / m), side = m <= ncols ? m : ncols;
-    const double* gsrc = w.g + (int64_t)b * g2;
-    for (int e = lane; e < side * side; e += 32) G[e] = gsrc[e];
-    __syncwarp();
-    const double* Gf = jacobi_warp(G, Gn, V, side, cs, sn, pa, pb);
+    if (role == 0) {
+        const double* gsrc = w.g + (int64_t)b * g2;
+        for (int e = lane; e < side * side; e += 32) G[e] = gsrc[e];
+        __syncwarp();
+    }
+    const double* Gf = jacobi_pair(G, Gn, V, side, P, role, 1 + pair);
+    if (role == 1) {   // V is final: store it
+        double* vdst = w.v + (int64_t)b * g2;
+        for (int e = lane; e < side * side; e += 32) vdst[e] = V[e];
+        return;
+    }
     // eigenvalues, descending stable order
     if (lane < side) lam[lane] = fmax(Gf[lane * side + lane], 0.0);
     __syncwarp();
@@ -594,8 +625,6 @@ __global__ void __launch_bounds__(32 * kJacWarps) ttsvd_jacobi_kernel(const Ttsv
         }
         rk[n + 1] = R;
     }
-    double* vdst = w.v + (int64_t)b * g2;
-    for (int e = lane; e < side * side; e += 32) vdst[e] = V[e];
     if (lane < side) {
         w.lam[(int64_t)b * a.gmax + lane] = lam[lane];
         w.ord[(int64_t)b * a.gmax + lane] = ord[lane];
@@ -758,7 +787,7 @@ cudaError_t launch_ttsvd(const TtsvdArgs& a, size_t smem_bytes, cudaStream_t s) 
 cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStream_t s) {
     const int gm = a.gmax;
     const size_t smem_first = sizeof(double) * 32 + sizeof(double) * (size_t)((a.elems + 1) / 2);
-    const size_t smem_jac = (sizeof(double) * (size_t)(3 * gm * gm + 2 * 16 + 32) + sizeof(int) * 96) * kJacWarps;
+    const size_t smem_jac = (sizeof(double) * (size_t)(3 * gm * gm + 32) + sizeof(JacParams)) * kJacPairs;
     const size_t smem_step = sizeof(double) * (size_t)(gm * gm + gm) + sizeof(int) * (size_t)((gm + 3) & ~3) +
                              2 * sizeof(int64_t) + 2 * sizeof(float) * (size_t)a.elems;
     cudaError_t e;
@@ -771,7 +800,7 @@ cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStre
     if ((e = cudaFuncSetAttribute(ttsvd_step_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
     ttsvd_first_kernel<<<a.B, kThreads, smem_first, s>>>(a, w);
     for (int n = 0; n + 1 < a.N; ++n) {
-        ttsvd_jacobi_kernel<<<(a.B + kJacWarps - 1) / kJacWarps, 32 * kJacWarps, smem_jac, s>>>(a, w, n);
+        ttsvd_jacobi_kernel<<<(a.B + kJacPairs - 1) / kJacPairs, 64 * kJacPairs, smem_jac, s>>>(a, w, n);
         ttsvd_step_kernel<<<a.B, kThreads, smem_step, s>>>(a, w, n);
     }
     return cudaGetLastError();
