@@ -218,7 +218,8 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     const bool uniform = hx.uniform && hy.uniform && hx.urank == hy.urank;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    // TTC_KERNEL=generic|fast|wpp forces the general-shape / CTA-per-pair / warp-per-pair tensor-core kernel (cross-checks)
+    // TTC_KERNEL=generic|fast|wpp|small forces the general-shape / CTA-per-pair / warp-per-pair tensor-core /
+    // tiny-batch kernel (cross-checks)
     const char* kv = std::getenv("TTC_KERNEL");
     const bool force_generic = kv && std::strcmp(kv, "generic") == 0;
     // uniform rank-16 trains with 16-byte aligned cores and trains: the specialised rank-16 kernel
@@ -231,6 +232,32 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     const bool force_fast = kv && std::strcmp(kv, "fast") == 0;
     const bool force_wpp = kv && std::strcmp(kv, "wpp") == 0;
     const bool uniform_r64 = uniform && hx.urank == 64 && aligned16 && (hx.train_elems_uniform & 3) == 0;
+    // tiny batches are latency-bound: both trains of a pair staged at once, one DRAM round trip per pair
+    // (TTC_KERNEL=small forces it for any batch that fits, for cross-checks)
+    const bool force_small = kv && std::strcmp(kv, "small") == 0;
+    if ((B <= 4 && !kv) || force_small) {
+        ttc::SmallLayout L{0, 0, 1, 1};
+        for (int b = 0; b < B; ++b) {
+            int64_t xe = 0, ye = 0;
+            for (int n = 0; n < a.N; ++n) {
+                const int64_t R = hx.rank(b, n), S = hx.rank(b, n + 1), P = hy.rank(b, n), Q = hy.rank(b, n + 1);
+                xe += R * a.dims[n] * S;
+                ye += P * a.dims[n] * Q;
+                L.wmax = (int32_t)std::max<int64_t>(L.wmax, R * a.dims[n] * Q);
+                L.zmax = (int32_t)std::max<int64_t>(L.zmax, S * Q);
+            }
+            L.xmax = (int32_t)std::max<int64_t>(L.xmax, (xe + 3) & ~int64_t(3));
+            L.ymax = (int32_t)std::max<int64_t>(L.ymax, (ye + 3) & ~int64_t(3));
+        }
+        L.wmax = (L.wmax + 3) & ~3;
+        L.zmax = (L.zmax + 3) & ~3;
+        const int64_t bytes = 4 * ((int64_t)L.xmax + L.ymax + L.wmax + 2 * (int64_t)L.zmax);
+        if (bytes <= 200 * 1024) {
+            e = ttc::launch_inner_small(a, L, s);
+            if (e != cudaSuccess) return cuda_fail(e, "ttc_inner launch");
+            return TTC_OK;
+        }
+    }
     if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
         e = ttc::launch_inner_r16(a, s);
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))

@@ -37,6 +37,11 @@ bool        inner_r64_supported(const InnerArgs& a, bool uniform_r64);
 bool        inner_wpp_supported(const InnerArgs& a, int max_rank);
 cudaError_t launch_inner_wpp(const InnerArgs& a, int max_rank, bool ranks_mult8, cudaStream_t s);
 cudaError_t launch_inner_r64(const InnerArgs& a, cudaStream_t s);
+// tiny batches (inner_small.cu): both trains of a pair in SMEM at once; floats of each region
+struct SmallLayout {
+    int32_t xmax, ymax, wmax, zmax;
+};
+cudaError_t launch_inner_small(const InnerArgs& a, const SmallLayout& L, cudaStream_t s);
 bool        inner_ffma_supported(const InnerArgs& a, int max_rank, bool ranks_mult8);
 cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s);
 

@@ -198,7 +198,7 @@ def test_uniform_rank16_shapes(dims):
     _check(X, X, got, range(B), "self")
 
 
-@pytest.mark.parametrize("variant", ["generic", "fast", "wpp"])
+@pytest.mark.parametrize("variant", ["generic", "fast", "wpp", "small"])
 def test_kernel_variants_agree(monkeypatch, variant):
     """Every tt_inner kernel (default dispatch vs TTC_KERNEL=generic / fast / wpp) agrees within fp32 rounding."""
     for cfg, B in (("C2", 16), ("C5", 24), ("C1", 1), ("C4", 2)):
