@@ -14,25 +14,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// Division by a runtime constant d >= 1 for 0 <= n < 2^31 without the integer-divide sequence
-// (Granlund-Montgomery): q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = 2^32 (2^l - d) / d + 1.
-struct FastDiv {
-    uint32_t d, m, l;
-    __device__ __forceinline__ void init(uint32_t dd) {
-        d = dd;
-        l = 0;
-        while ((1u << l) < d) ++l;
-        m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << l) - d)) / d + 1);
-    }
-    __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> l; }
-};
-
 struct PairCtx {
     int32_t rx[kMaxContractOrder + 1], ry[kMaxContractOrder + 1];
     int64_t xo[kMaxContractOrder + 1], yo[kMaxContractOrder + 1];   // core offsets within the train
     int32_t orr[kMaxLadder + 1];                                     // output bond ranks
     int64_t oo[kMaxLadder + 1];                                      // output core offsets within the pair
-    FastDiv fd[4];   // divisors of the core being emitted: quads per column, I, right-bond split, H
 };
 
 __device__ __forceinline__ void st_cs4(float* p, float a, float b, float c, float d) {
@@ -347,17 +333,7 @@ __global__ void __launch_bounds__(kThreads, 4) contract_kernel(const ContractArg
     for (int l = 0; l < a.L; ++l) {
         const OutCore& oc = a.outc[l];
         int rows, cols;
-        if (threadIdx.x < 4) {   // magic-number divisors of this core, one per thread
-            const LadderEl& el = a.seq[oc.el];
-            const bool xf = el.kind == EL_XFREE;
-            const int I = xf ? a.xdims[el.mode] : a.ydims[el.mode];
-            const int Rn = xf ? c.rx[el.mode + 1] : c.ry[el.mode + 1];
-            const int H = xf ? c.ry[el.hold] : c.rx[el.hold];
-            const int d = threadIdx.x == 0 ? (c.orr[l] >= 4 ? c.orr[l] / 4 : 1)
-                        : threadIdx.x == 1 ? I : threadIdx.x == 2 ? (xf ? Rn : H) : H;
-            c.fd[threadIdx.x].init((uint32_t)d);
-        }
-        __syncthreads();
+        __syncthreads();   // the staged trains (first core) / the previous core's buffers are ready / free
         if (oc.lt_count > 0) build_chain(a, c, xc, yc, oc.lt_first, oc.lt_count, TL, tmp, &rows, &cols);
         if (oc.rt_count > 0) {
             __syncthreads();

@@ -26,11 +26,9 @@
 namespace ttc {
 namespace {
 
-constexpr int kWarps = 8;
 #ifndef TTC_RM16_MAXNREG
 #define TTC_RM16_MAXNREG 96
 #endif
-constexpr int kThreads = 32 * kWarps;
 
 using namespace tc;
 

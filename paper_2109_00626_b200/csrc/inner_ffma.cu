@@ -92,12 +92,6 @@ __device__ __forceinline__ void dot4x2(unsigned long long& acc, const float4 a, 
     fma2(acc, pk(a.x, a.y), pk(b.x, b.y));
     fma2(acc, pk(a.z, a.w), pk(b.z, b.w));
 }
-__device__ __forceinline__ float dot4(float acc, const float4 a, const float4 b) {
-    acc = fmaf(a.x, b.x, acc);
-    acc = fmaf(a.y, b.y, acc);
-    acc = fmaf(a.z, b.z, acc);
-    return fmaf(a.w, b.w, acc);
-}
 
 // Copy `runs` runs of `run` floats (run % 4 == 0) from contiguous global memory into shared memory with a run
 // stride of run + kPad (run / 4 in [2, kMagicMax]): e / (run / 4) is one IMAD.HI with the magic table.

@@ -285,45 +285,7 @@ __global__ void __launch_bounds__(kThreads) ttsvd_kernel(const TtsvdArgs a) {
 //            in descending order, the delta-truncated rank R_n
 //   step   : (per step n) core n = U (R24 signs), Z_{n+1}, its Gram (or, after the last step, core N)
 
-// Gram matrix of Z (m x ncols, Z[r + m c]) of the smaller side, fp64, into g (side x side, row-major).
-// Rows side: a thread per entry (consecutive threads read consecutive rows of a column); columns side: a warp
-// per entry, lanes along the column (contiguous, conflict-free), shuffle-reduced.
-__device__ void gram_to(const float* Z, int m, int ncols, double* g) {
-    const bool rows_side = m <= ncols;
-    const int side = rows_side ? m : ncols;
-    if (rows_side) {
-        for (int e = threadIdx.x; e < side * side; e += blockDim.x) {
-            const int i = e / side, j = e - i * side;
-            if (j < i) continue;
-            double acc0 = 0.0, acc1 = 0.0;   // two chains: half the dependent-add latency
-            int c = 0;
-            for (; c + 1 < ncols; c += 2) {
-                acc0 += (double)Z[i + m * c] * Z[j + m * c];
-                acc1 += (double)Z[i + m * (c + 1)] * Z[j + m * (c + 1)];
-            }
-            if (c < ncols) acc0 += (double)Z[i + m * c] * Z[j + m * c];
-            g[i * side + j] = acc0 + acc1;
-            g[j * side + i] = acc0 + acc1;
-        }
-        return;
-    }
-    const int wp = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int e = wp; e < side * side; e += nw) {
-        const int i = e / side, j = e - i * side;
-        if (j < i) continue;
-        const float* zi = Z + m * i;
-        const float* zj = Z + m * j;
-        double acc = 0.0;
-        for (int r = l; r < m; r += 32) acc += (double)zi[r] * zj[r];
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (l == 0) {
-            g[i * side + j] = acc;
-            g[j * side + i] = acc;
-        }
-    }
-}
-
-// The same Gram matrix as register-tiled fp64 products: 4 x 4 tiles of the upper triangle, one warp per tile,
+// Gram matrix of Z (m x ncols, Z[r + m c]) of the smaller side (side x side, row-major) in fp64 register tiles: 4 x 4 tiles of the upper triangle, one warp per tile,
 // its lanes splitting the summed index (lane, lane + 32, ...), the 16 partial sums reduced by warp shuffles (no
 // atomics), then written to g and mirrored.  Element (i, t) of the side x len operand is Z[i si + t st].
 __device__ void gram_tiled(const float* Z, int m, int ncols, double* g) {
