@@ -70,13 +70,19 @@ __global__ void __launch_bounds__(kThreads) inner_small_kernel(const InnerArgs a
             W[e] = acc;
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < S * Q; e += blockDim.x) {    // Z'[s + S q]: K = (r, i) contiguous in both
+        // Z'[s + S q] = sum_k X[k + RI s] W[k + RI q] (K = (r, i) contiguous in both): 8 lanes per output split
+        // k and combine by shuffles (a short dependent chain instead of RI serial FMAs); fixed order
+        for (int e0 = threadIdx.x >> 3; e0 < ((S * Q + 3) & ~3); e0 += blockDim.x >> 3) {
+            const int sub = threadIdx.x & 7, e = min(e0, S * Q - 1);
             const int q = e / S, s = e - q * S;
             const float* x = X + RI * s;
             const float* w = W + RI * q;
             float acc = 0.f;
-            for (int k = 0; k < RI; ++k) acc = fmaf(x[k], w[k], acc);
-            Zn[e] = acc;
+            for (int k = sub; k < RI; k += 8) acc = fmaf(x[k], w[k], acc);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            if (sub == 0 && e0 < S * Q) Zn[e] = acc;
         }
         __syncthreads();
         float* t = Z; Z = Zn; Zn = t;
