@@ -324,8 +324,12 @@ def main():
         alg_bytes = float(byts.sum())
         alg_flops = 2.0 * float(mac.sum())
 
+        # heterogeneous pair costs (C5's random ranks): a cost-descending work list, computed once per batch like a
+        # plan (host sort of ttc_pair_cost), so the most expensive pairs start first and the tail is short
+        order = ttc.ttc_cost_order(XD, YD) if len(set(np.round(mac, 3))) > 1 else None
+
         def step():
-            ttc.ttc_inner(XD, YD, out=out, stream=stream)
+            ttc.ttc_inner(XD, YD, out=out, stream=stream, order=order)
         kernel_name = "inner"
 
     xin = X.cores if hasattr(X, "cores") else X    # the step's device inputs (cores, or dense tensors for alg2)

@@ -86,6 +86,14 @@ typedef struct {
  * ------------------------------------------------------------------------------------------------- */
 ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_dev, void* stream);
 
+/* ttc_inner with a processing order (a cost-descending work list, so that the batch's
+ * most expensive pairs start first and heterogeneous-rank batches such as C5 end with a short tail).  The
+ * results are identical (bitwise) to ttc_inner's: out_dev[b] is still pair b's value.
+ *   order_host: host int32 [B], a permutation of 0..B-1 (validated: else TTC_ERR_ARG); order_dev: its device
+ *   copy (caller-owned, read by the kernels).  ttc_pair_cost gives the cost to sort by. */
+ttc_status ttc_inner_ordered(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_t* order_host,
+                             const int32_t* order_dev, float* out_dev, void* stream);
+
 /* ---------------------------------------------------------------------------------------------------
  * Partial contraction (TTCP, Alg. 2) of pair b: Z_b = X_b x_{(n_1,m_1),...,(n_K,m_K)} Y_b
  * (Eq. 8, applied to each of K disjoint mode pairs), returned in TT format

@@ -33,7 +33,7 @@ TTC_OK, TTC_ERR_NULL, TTC_ERR_SHAPE, TTC_ERR_RANK, TTC_ERR_MODES = 0, 1, 2, 3, 4
 TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG = 5, 6, 7, 8, 9
 TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
 
-EXPORTED = ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
+EXPORTED = ("ttc_inner", "ttc_inner_ordered", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
             "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity", "ttc_tt_svd_workspace",
             "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
             "ttc_last_error", "ttc_version")
@@ -48,6 +48,8 @@ class ttc_tt_batch(ctypes.Structure):
 
 _P = ctypes.POINTER
 _lib.ttc_inner.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_inner_ordered.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p]
 _lib.ttc_contract_plan_create.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_int32, ctypes.c_void_p,
                                           ctypes.c_void_p, _P(ctypes.c_void_p)]
 _lib.ttc_splice_plan_create.argtypes = [_P(ttc_tt_batch), _P(ttc_tt_batch), ctypes.c_int32, ctypes.c_int32,
@@ -71,7 +73,7 @@ _lib.ttc_tt_svd_workspace.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_v
 _lib.ttc_tt_svd.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                             ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                             ctypes.c_void_p]
-for _f in ("ttc_inner", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
+for _f in ("ttc_inner", "ttc_inner_ordered", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
            "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity",
            "ttc_tt_svd_workspace", "ttc_contract", "ttc_pair_cost", "ttc_partition"):
     getattr(_lib, _f).restype = ctypes.c_int
@@ -200,12 +202,30 @@ def _stream_handle(stream) -> Optional[int]:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def ttc_inner(x: TTDevice, y: TTDevice, out: torch.Tensor = None, stream=None) -> torch.Tensor:
-    """out[b] = <X_b, Y_b> (ttc.h: ttc_inner).  Asynchronous on `stream` (default: torch's current stream)."""
+class CostOrder:
+    """A processing order for ttc_inner_ordered: pairs by descending ttc_pair_cost (MACs), host + device copy."""
+
+    def __init__(self, x: "TTDevice", y: "TTDevice"):
+        mac, _ = ttc_pair_cost(x, y)
+        self.host = np.ascontiguousarray(np.argsort(-mac, kind="stable").astype(np.int32))
+        self.dev = torch.from_numpy(self.host).to(x.cores.device)
+
+
+def ttc_cost_order(x: "TTDevice", y: "TTDevice") -> CostOrder:
+    return CostOrder(x, y)
+
+
+def ttc_inner(x: TTDevice, y: TTDevice, out: torch.Tensor = None, stream=None, order: CostOrder = None) -> torch.Tensor:
+    """out[b] = <X_b, Y_b> (ttc.h: ttc_inner; with `order`, ttc_inner_ordered: same values, pairs started in
+    that order).  Asynchronous on `stream` (default: torch's current stream)."""
     if out is None:
         out = torch.empty(x.B, dtype=torch.float32, device=x.cores.device)
-    _check(_lib.ttc_inner(ctypes.byref(x.c), ctypes.byref(y.c), _ptr(out) if out.numel() else None,
-                          _stream_handle(stream)))
+    if order is None:
+        _check(_lib.ttc_inner(ctypes.byref(x.c), ctypes.byref(y.c), _ptr(out) if out.numel() else None,
+                              _stream_handle(stream)))
+    else:
+        _check(_lib.ttc_inner_ordered(ctypes.byref(x.c), ctypes.byref(y.c), _ptr(order.host), _ptr(order.dev),
+                                      _ptr(out) if out.numel() else None, _stream_handle(stream)))
     return out
 
 

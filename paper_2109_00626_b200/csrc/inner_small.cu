@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kThreads) inner_small_kernel(const InnerArgs a
     extern __shared__ __align__(16) float sm[];
     __shared__ int32_t rx[TTC_MAX_ORDER + 1], ry[TTC_MAX_ORDER + 1];
     __shared__ int64_t xo[TTC_MAX_ORDER + 1], yo[TTC_MAX_ORDER + 1];
-    const int b = blockIdx.x, N = a.N;
+    const int b = a.order ? a.order[blockIdx.x] : (int)blockIdx.x, N = a.N;
     for (int k = threadIdx.x; k <= N; k += blockDim.x) {
         rx[k] = a.x.ranks ? a.x.ranks[(int64_t)b * (N + 1) + k] : ((k == 0 || k == N) ? 1 : a.x.urank);
         ry[k] = a.y.ranks ? a.y.ranks[(int64_t)b * (N + 1) + k] : ((k == 0 || k == N) ? 1 : a.y.urank);

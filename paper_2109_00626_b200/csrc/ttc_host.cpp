@@ -187,8 +187,37 @@ const char* ttc_last_error(void) { return g_last_error.c_str(); }
 
 int32_t ttc_version(void) { return TTC_VERSION_MAJOR * 100 + TTC_VERSION_MINOR; }
 
+namespace {
+ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_t* order_dev, float* out_dev,
+                      void* stream);
+}  // namespace
+
 ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_dev, void* stream) {
     g_last_error.clear();
+    return inner_impl(x, y, nullptr, out_dev, stream);
+}
+
+ttc_status ttc_inner_ordered(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_t* order_host,
+                             const int32_t* order_dev, float* out_dev, void* stream) {
+    g_last_error.clear();
+    if (!x || !y) return fail(TTC_ERR_NULL, "X / Y batch descriptor is NULL");
+    const int B = x->batch;
+    if (B > 0) {
+        if (!order_host || !order_dev) return fail(TTC_ERR_NULL, "order_host / order_dev is NULL");
+        std::vector<char> seen((size_t)B, 0);
+        for (int k = 0; k < B; ++k) {
+            const int32_t v = order_host[k];
+            if (v < 0 || v >= B || seen[(size_t)v])
+                return fail(TTC_ERR_ARG, "order[%d] = %d: order must be a permutation of 0..%d", k, v, B - 1);
+            seen[(size_t)v] = 1;
+        }
+    }
+    return inner_impl(x, y, order_dev, out_dev, stream);
+}
+
+namespace {
+ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_t* order_dev, float* out_dev,
+                      void* stream) {
     HostTrain hx, hy;
     ttc_status st;
     if ((st = check_batch(x, "X", TTC_MAX_ORDER, &hx)) != TTC_OK) return st;
@@ -211,7 +240,7 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     a.x = to_dev(hx);
     a.y = to_dev(hy);
     a.out = out_dev;
-    a.order = nullptr;
+    a.order = order_dev;   // nullptr: natural order
     const int mr = std::max(hx.max_rank, hy.max_rank);
     a.zmax = mr * mr;
     a.wbuf = std::max(mr * mr, 8192);
@@ -273,6 +302,7 @@ ttc_status ttc_inner(const ttc_tt_batch* x, const ttc_tt_batch* y, float* out_de
     if (e != cudaSuccess) return cuda_fail(e, "ttc_inner launch");
     return TTC_OK;
 }
+}  // namespace
 
 ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
                            void* stream) {

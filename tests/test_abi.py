@@ -28,7 +28,7 @@ def _declared_symbols():
 
 def test_library_exports_every_declared_symbol():
     syms = _declared_symbols()
-    assert len(syms) == 16
+    assert len(syms) == 17
     lib = ctypes.CDLL(ttc.LIB_PATH)
     for s in syms:
         assert hasattr(lib, s), s
@@ -289,3 +289,17 @@ def test_tt_svd_workspace_sizes():
     assert ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(2, 1)) > 0
     with pytest.raises(ttc.TTCError):
         ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(1, 1))
+
+
+def test_inner_ordered_validates_the_permutation():
+    """ttc_inner_ordered checks its host order on the host (no CUDA call on error)."""
+    import ctypes
+    X, Y = ttgen.config_batch("C2", kind="iid", B=4)
+    XD, YD = ttc.TTDevice.from_batch(X, "cpu"), ttc.TTDevice.from_batch(Y, "cpu")
+    out = torch.zeros(4)
+    for bad in ([0, 1, 2, 2], [0, 1, 2, 4], [-1, 0, 1, 2]):
+        o = np.asarray(bad, np.int32)
+        rc = ttc._lib.ttc_inner_ordered(ctypes.byref(XD.c), ctypes.byref(YD.c), ttc._ptr(o), ttc._ptr(o),
+                                         ttc._ptr(out), None)
+        assert rc == ttc.TTC_ERR_ARG, bad
+        assert "permutation" in ttc.ttc_last_error()

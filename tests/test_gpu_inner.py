@@ -265,3 +265,15 @@ def test_ffma_rank_mult8_shapes(case):
     Xu = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, ur, dims, "geo")
     got = _run(Xu, Xu)
     _check(Xu, Xu, got, _sample(B, 24, case + 2), "self")
+
+
+def test_cost_ordered_inner_is_bitwise_equal():
+    """ttc_inner_ordered (cost-descending work list) returns exactly ttc_inner's values, pair by pair."""
+    for cfg, B in (("C5", 300), ("C2", 40), ("C1", 3), ("C4", 6)):
+        X, Y = ttgen.config_batch(cfg, kind="corr", B=B)
+        XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+        ref = ttc.ttc_inner(XD, YD).cpu().numpy()
+        order = ttc.ttc_cost_order(XD, YD)
+        assert sorted(order.host.tolist()) == list(range(B))
+        got = ttc.ttc_inner(XD, YD, order=order).cpu().numpy()
+        assert np.array_equal(ref.view(np.uint32), got.view(np.uint32)), cfg
