@@ -957,7 +957,7 @@ ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const
         const int64_t sx = (max_elems(hx) + 3) & ~int64_t(3), sy = (max_elems(hy) + 3) & ~int64_t(3);
         sa.k4 = (int32_t)((p->k_floats + 3) & ~int64_t(3));
         size_t smem = sizeof(float) * (size_t)sa.k4;
-        if (4 * (sx + sy) + smem <= 48 * 1024) {
+        if (4 * (sx + sy) + smem <= 110 * 1024) {   // (2 CTAs per SM at the limit)
             sa.stage_x = (int32_t)sx;
             sa.stage_y = (int32_t)sy;
             smem += 4 * (size_t)(sx + sy);
