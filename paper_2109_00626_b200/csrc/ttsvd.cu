@@ -12,6 +12,7 @@
 // ranks at ranks_dev[b * (N + 1)].
 #include <cfloat>
 
+#include "tc_common.cuh"
 #include "ttc_internal.h"
 
 namespace ttc {
@@ -336,7 +337,12 @@ __device__ void gram_tiled(const float* Z, int m, int ncols, double* g) {
 
 // Z[dst(e)] = src[e] for the tensor's elements e = tid, tid + blockDim, ... read contiguously; dst by the
 // mixed-radix walk of e (radices rad, X^rho strides dstr, source mode order) advanced by blockDim's digits with
-// carries (NW >= N digits in registers; NW = 0: per-element division).  Returns this thread's sum of squares.
+// carries (NW >= N digits in registers; NW = 0: per-element division).  The copies are cp.async (all in flight
+// at once); the caller waits for them.
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
 template <int NW>
 __device__ __forceinline__ double scatter_walk(const TtsvdArgs& a, const float* src, float* Z, const int32_t* rad_s,
                                                const int32_t* dstr_s) {
@@ -346,9 +352,7 @@ __device__ __forceinline__ double scatter_walk(const TtsvdArgs& a, const float* 
         for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
             int q = e, off = 0;
             for (int p = 0; p < N; ++p) { off += (q % rad_s[p]) * dstr_s[p]; q /= rad_s[p]; }
-            const float v = __ldg(src + e);
-            Z[off] = v;
-            nrm += (double)v * v;
+            cp_async4(Z + off, src + e);
         }
         return nrm;
     }
@@ -364,9 +368,7 @@ __device__ __forceinline__ double scatter_walk(const TtsvdArgs& a, const float* 
         off += dig[p] * dstr[p];
     }
     for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
-        const float v = __ldg(src + e);
-        Z[off] = v;
-        nrm += (double)v * v;
+        cp_async4(Z + off, src + e);
         int carry = 0;
 #pragma unroll
         for (int p = 0; p < W; ++p) {   // (padding digits: radix 1, stride 0 -> no effect)
@@ -410,9 +412,17 @@ __global__ void __launch_bounds__(kThreads, 4) ttsvd_first_kernel(const TtsvdArg
         }
     }
     __syncthreads();
-    double nrm = N <= 4 ? scatter_walk<4>(a, src, Z, rad, dstr) : scatter_walk<0>(a, src, Z, rad, dstr);
-    nrm = block_sum(nrm, red);   // (its barriers also publish Z)
-    for (int e = threadIdx.x; e < a.elems; e += blockDim.x) zg[e] = Z[e];
+    if (N <= 4) scatter_walk<4>(a, src, Z, rad, dstr);
+    else scatter_walk<0>(a, src, Z, rad, dstr);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    double nrm = 0.0;   // ||X||^2, and Z_0 to the workspace for the step kernel
+    for (int e = threadIdx.x; e < a.elems; e += blockDim.x) {
+        const float v = Z[e];
+        zg[e] = v;
+        nrm += (double)v * v;
+    }
+    nrm = block_sum(nrm, red);
     if (threadIdx.x == 0) {
         w.nrm[b] = nrm;
         a.ranks[(int64_t)b * (N + 1)] = 1;
@@ -614,13 +624,28 @@ __global__ void __launch_bounds__(kThreads, 3) ttsvd_step_kernel(const TtsvdArgs
         for (int k = 0; k < n; ++k) o += (int64_t)rk[k] * a.dims[k] * rk[k + 1];
         oo[0] = o;
     }
+    // Z_n and the eigenvectors: every load in flight at once (16-byte cp.async where aligned), one round trip
     const float* zg = w.z + (int64_t)b * a.elems;
-    for (int e = threadIdx.x; e < (int)cur; e += blockDim.x) Z[e] = zg[e];
-    for (int e = threadIdx.x; e < side * side; e += blockDim.x) V[e] = w.v[(int64_t)b * gm * gm + e];
+    const double* vg = w.v + (int64_t)b * gm * gm;
+    const int nz = (int)cur;
+    if (((reinterpret_cast<uintptr_t>(zg) | reinterpret_cast<uintptr_t>(Z)) & 15u) == 0) {
+        for (int e = threadIdx.x; e < (nz >> 2); e += blockDim.x) tc::cp_async16(Z + 4 * e, zg + 4 * e);
+        for (int e = (nz & ~3) + threadIdx.x; e < nz; e += blockDim.x) Z[e] = zg[e];
+    } else {
+        for (int e = threadIdx.x; e < nz; e += blockDim.x) Z[e] = zg[e];
+    }
+    if (((reinterpret_cast<uintptr_t>(vg) | reinterpret_cast<uintptr_t>(V)) & 15u) == 0) {
+        for (int e = threadIdx.x; e < (side * side >> 1); e += blockDim.x) tc::cp_async16(V + 2 * e, vg + 2 * e);
+        if ((side * side) & 1) if (threadIdx.x == 0) V[side * side - 1] = vg[side * side - 1];
+    } else {
+        for (int e = threadIdx.x; e < side * side; e += blockDim.x) V[e] = vg[e];
+    }
+    tc::cp_commit_group();
     for (int j = threadIdx.x; j < side; j += blockDim.x) {
         lam[j] = w.lam[(int64_t)b * gm + j];
         ord[j] = w.ord[(int64_t)b * gm + j];
     }
+    tc::cp_wait_pending(0);
     __syncthreads();
     float* out = a.cores + (int64_t)b * a.train_cap + oo[0];
     // ---- U (m x R)
