@@ -284,6 +284,25 @@ __device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* 
     }
 }
 
+__device__ __forceinline__ void cp_async4_(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16_(float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+// Contiguous copy of n floats global -> shared with cp.async (16-byte pieces when both ends are aligned); the
+// caller waits (cp.async.wait_all) and synchronises.
+__device__ __forceinline__ void stage_async(float* dst, const float* src, int n) {
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u) == 0) {
+        for (int e = threadIdx.x; e < (n >> 2); e += blockDim.x) cp_async16_(dst + 4 * e, src + 4 * e);
+        for (int e = (n & ~3) + threadIdx.x; e < n; e += blockDim.x) cp_async4_(dst + e, src + e);
+    } else {
+        for (int e = threadIdx.x; e < n; e += blockDim.x) cp_async4_(dst + e, src + e);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 4) contract_kernel(const ContractArgs a) {
     extern __shared__ float scratch[];
     __shared__ PairCtx c;
@@ -325,8 +344,9 @@ __global__ void __launch_bounds__(kThreads, 4) contract_kernel(const ContractArg
     if (a.stage_floats > 0 && nx + ny <= a.stage_floats) {
         float* sx = scratch + a.stage_off;
         float* sy = sx + nx;
-        for (int64_t e = threadIdx.x; e < nx; e += blockDim.x) sx[e] = __ldg(xg + e);
-        for (int64_t e = threadIdx.x; e < ny; e += blockDim.x) sy[e] = __ldg(yg + e);
+        stage_async(sx, xg, (int)nx);   // every load of both trains in flight at once (one round trip)
+        stage_async(sy, yg, (int)ny);
+        asm volatile("cp.async.wait_all;" ::: "memory");
         xc = sx;
         yc = sy;
     }
