@@ -446,6 +446,41 @@ struct JacParams {
 };
 __device__ __forceinline__ void pair_bar(int bar) { asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory"); }
 
+// One round's two-sided rotation of G into Gn for this lane's upper-triangle 2 x 2 blocks (bp: q1 << 8 | q2, -1
+// past the end), mirrored.  G and Gn are distinct buffers (__restrict__): every block's loads can be issued
+// ahead of the other blocks' stores.
+__device__ __forceinline__ void block_update(const double* __restrict__ G, double* __restrict__ Gn, int n,
+                                             const JacParams& P, int cur, const int (&bp)[5]) {
+    double y[5][4];
+    int a1s[5], b1s[5], a2s[5], b2s[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+        if (bp[u] < 0) break;
+        const int q1 = bp[u] >> 8, q2 = bp[u] & 255;
+        const int a1 = P.pa[cur][q1], b1 = P.pb[cur][q1], a2 = P.pa[cur][q2], b2 = P.pb[cur][q2];
+        const double c1 = P.cs[cur][q1], s1 = P.sn[cur][q1], c2 = P.cs[cur][q2], s2 = P.sn[cur][q2];
+        const bool hb1 = b1 < n, hb2 = b2 < n;
+        const double g00 = G[a1 * n + a2], g01 = hb2 ? G[a1 * n + b2] : 0.0;
+        const double g10 = hb1 ? G[b1 * n + a2] : 0.0, g11 = hb1 && hb2 ? G[b1 * n + b2] : 0.0;
+        const double x00 = c2 * g00 - s2 * g01, x01 = s2 * g00 + c2 * g01;   // B J2
+        const double x10 = c2 * g10 - s2 * g11, x11 = s2 * g10 + c2 * g11;
+        y[u][0] = c1 * x00 - s1 * x10; y[u][1] = c1 * x01 - s1 * x11;     // J1^T (B J2)
+        y[u][2] = s1 * x00 + c1 * x10; y[u][3] = s1 * x01 + c1 * x11;
+        a1s[u] = a1; b1s[u] = b1; a2s[u] = a2; b2s[u] = b2;
+    }
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+        if (bp[u] < 0) break;
+        const int a1 = a1s[u], b1 = b1s[u], a2 = a2s[u], b2 = b2s[u];
+        const bool hb1 = b1 < n, hb2 = b2 < n;
+        Gn[a1 * n + a2] = y[u][0];
+        Gn[a2 * n + a1] = y[u][0];
+        if (hb2) { Gn[a1 * n + b2] = y[u][1]; Gn[b2 * n + a1] = y[u][1]; }
+        if (hb1) { Gn[b1 * n + a2] = y[u][2]; Gn[a2 * n + b1] = y[u][2]; }
+        if (hb1 && hb2) { Gn[b1 * n + b2] = y[u][3]; Gn[b2 * n + b1] = y[u][3]; }
+    }
+}
+
 __device__ double* jacobi_pair(double* G, double* Gn, double* V, int n, JacParams& P, int role, int bar) {
     const int lane = threadIdx.x & 31;
     const int np = (n + 1) & ~1, half = np / 2;
@@ -500,25 +535,7 @@ __device__ double* jacobi_pair(double* G, double* Gn, double* V, int n, JacParam
             pair_bar(bar);   // round r's rotations published; the V warp has finished round r - 1
             if (stop) break;
             if (rr) {
-#pragma unroll
-                for (int u = 0; u < 5; ++u) {
-                    if (bp[u] < 0) break;
-                    const int q1 = bp[u] >> 8, q2 = bp[u] & 255;
-                    const int a1 = P.pa[cur][q1], b1 = P.pb[cur][q1], a2 = P.pa[cur][q2], b2 = P.pb[cur][q2];
-                    const double c1 = P.cs[cur][q1], s1 = P.sn[cur][q1], c2 = P.cs[cur][q2], s2 = P.sn[cur][q2];
-                    const bool hb1 = b1 < n, hb2 = b2 < n;
-                    const double g00 = G[a1 * n + a2], g01 = hb2 ? G[a1 * n + b2] : 0.0;
-                    const double g10 = hb1 ? G[b1 * n + a2] : 0.0, g11 = hb1 && hb2 ? G[b1 * n + b2] : 0.0;
-                    const double x00 = c2 * g00 - s2 * g01, x01 = s2 * g00 + c2 * g01;
-                    const double x10 = c2 * g10 - s2 * g11, x11 = s2 * g10 + c2 * g11;
-                    const double y00 = c1 * x00 - s1 * x10, y01 = c1 * x01 - s1 * x11;
-                    const double y10 = s1 * x00 + c1 * x10, y11 = s1 * x01 + c1 * x11;
-                    Gn[a1 * n + a2] = y00;
-                    Gn[a2 * n + a1] = y00;
-                    if (hb2) { Gn[a1 * n + b2] = y01; Gn[b2 * n + a1] = y01; }
-                    if (hb1) { Gn[b1 * n + a2] = y10; Gn[a2 * n + b1] = y10; }
-                    if (hb1 && hb2) { Gn[b1 * n + b2] = y11; Gn[b2 * n + b1] = y11; }
-                }
+                block_update(G, Gn, n, P, cur, bp);
                 __syncwarp();
                 double* tmp = G; G = Gn; Gn = tmp;
             }
