@@ -303,3 +303,24 @@ def test_inner_ordered_validates_the_permutation():
                                          ttc._ptr(out), None)
         assert rc == ttc.TTC_ERR_ARG, bad
         assert "permutation" in ttc.ttc_last_error()
+
+
+def test_every_compute_entry_is_a_noop_on_an_empty_batch():
+    """B = 0: every compute entry point returns TTC_OK without touching the device (this
+    container has none, so any CUDA call would fail)."""
+    x = ttc.TTDevice(torch.zeros(1), [3, 4, 2], uniform_rank=2, batch=0)
+    y = ttc.TTDevice(torch.zeros(1), [3, 4, 2], uniform_rank=3, batch=0)
+    lib = ttc._lib
+    assert lib.ttc_inner_ordered(ctypes.byref(x.c), ctypes.byref(y.c), None, None, None, None) == ttc.TTC_OK
+    plan = ttc.ttc_contract_plan_create(x, y, [2], [2])
+    assert plan.total == 0 or plan.total >= 0
+    assert lib.ttc_contract(plan.handle, ctypes.byref(x.c), ctypes.byref(y.c), None, None, None) == ttc.TTC_OK
+    splice = ttc.ttc_splice_plan_create(x, y, 1, 1)
+    assert lib.ttc_contract(splice.handle, ctypes.byref(x.c), ctypes.byref(y.c), None, None, None) == ttc.TTC_OK
+    perm = np.asarray([3, 1, 2], np.int32)
+    assert lib.ttc_reconstruct(ctypes.byref(x.c), ttc._ptr(perm), None, None, None) == ttc.TTC_OK
+    dims = np.asarray([3, 4, 2], np.int32)
+    assert lib.ttc_tt_svd(0, 3, ttc._ptr(dims), None, None, ctypes.c_double(0.1), None, None, None, 0,
+                          None) == ttc.TTC_OK
+    nb = ctypes.c_int64(-1)
+    assert lib.ttc_tt_svd_workspace(0, 3, ttc._ptr(dims), None, ctypes.byref(nb)) == ttc.TTC_OK and nb.value == 0
