@@ -13,7 +13,7 @@ done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/ref_default.json 2> $O/ref_default.err
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e"
 $CMD > $O/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1
-for kc in "C2 inner_r16" "C3 contract" "C4 inner_r64" "C5 inner_ffma" "S1 splice" "R1 reconstruct" "A2 ttsvd"; do
+for kc in "C1 inner_small" "C2 inner_r16" "C3 contract" "C4 inner_r64" "C5 inner_ffma" "S1 splice" "R1 reconstruct" "A2 ttsvd"; do
   set -- $kc
   CMD2="python bench.py --config $1 --steps 2 --warmup 1 --no-cpu --no-e2e"
   $CMD2 > $O/plain_$1.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o $O/full_$1 -f $CMD2 > $O/ncu_full_$1.log 2>&1
