@@ -1,5 +1,7 @@
 // ttsvd.cu -- batched TT-SVD (ttc.h: ttc_tt_svd; Alg. 1), optionally of the permuted tensor
-// X^rho of Alg. 2 step 1.  One CTA per tensor, the whole tensor in shared memory:
+// X^rho of Alg. 2 step 1.  The method, as both implementations below compute it (the fused
+// one-CTA-per-tensor ttsvd_kernel, and the launch pipeline further down that ttc_tt_svd uses when a workspace
+// is given and every Gram side is <= 32):
 //   delta^2 = eps^2 / (N - 1) ||X||_F^2;  Z <- X_(1)
 //   for n = 1 .. N-1:  delta-truncated SVD of Z (R_{n-1} I_n x rest) through the eigenproblem of its smaller
 //                      Gram matrix (fp64, cyclic Jacobi with round-robin parallel rotations):
