@@ -70,7 +70,8 @@ typedef struct {
     const int64_t* offsets_host;  /* host [B] element offset of train b; NULL => packed                  */
     const int64_t* offsets_dev;   /* device copy of offsets_host (required iff offsets_host != NULL)     */
     const float*   cores;         /* device fp32 core values (see DATA MODEL)                           */
-    int64_t        n_elems;       /* number of floats addressable at `cores`; every train must fit      */
+    int64_t        n_elems;       /* number of floats addressable at `cores` (>= 1 when batch > 0, else
+                                     TTC_ERR_ARG); every train must fit in [0, n_elems)                 */
 } ttc_tt_batch;
 
 /* ---------------------------------------------------------------------------------------------------

@@ -220,6 +220,7 @@ def ttc_inner(x: TTDevice, y: TTDevice, out: torch.Tensor = None, stream=None, o
     that order).  Asynchronous on `stream` (default: torch's current stream)."""
     if out is None:
         out = torch.empty(x.B, dtype=torch.float32, device=x.cores.device)
+        _keep_alive(stream, out.device, out)
     if order is None:
         _check(_lib.ttc_inner(ctypes.byref(x.c), ctypes.byref(y.c), _ptr(out) if out.numel() else None,
                               _stream_handle(stream)))
@@ -341,6 +342,26 @@ def _svd_workspace(B, d, pm, device, workspace):
     return torch.empty(max(nb, 16), dtype=torch.uint8, device=device) if nb else None
 
 
+def _torch_stream(stream, device):
+    """The torch.cuda.Stream the call is enqueued on (the current stream when None)."""
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(stream), device=device)
+
+
+def _keep_alive(stream, device, *tensors):
+    """Tensors allocated here and used by kernels on `stream`: tell torch's caching allocator, so that their memory
+    is not handed to another allocation before the kernels on `stream` are done with it."""
+    if not torch.cuda.is_available():
+        return
+    ts = _torch_stream(stream, device)
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            t.record_stream(ts)
+
+
 def ttc_tt_svd_into(dense: torch.Tensor, dims, eps: float, cores: torch.Tensor, ranks: torch.Tensor, perm=None,
                     stream=None, workspace: torch.Tensor = None) -> None:
     """ttc_tt_svd into caller-owned device buffers (no host synchronisation): cores float32 [B * capacity],
@@ -354,6 +375,8 @@ def ttc_tt_svd_into(dense: torch.Tensor, dims, eps: float, cores: torch.Tensor, 
     _check(_lib.ttc_tt_svd(int(B), int(d.size), _ptr(d), _ptr(dense) if dense.numel() else None, _ptr(pm),
                            float(eps), _ptr(cores), _ptr(ranks), _ptr(ws) if ws is not None else None,
                            int(ws.numel()) if ws is not None else 0, _stream_handle(stream)))
+    if workspace is None:
+        _keep_alive(stream, dense.device, ws)
 
 
 def ttc_tt_svd(dense: torch.Tensor, dims, eps: float, perm=None, stream=None) -> "TTDevice":
@@ -371,7 +394,10 @@ def ttc_tt_svd(dense: torch.Tensor, dims, eps: float, perm=None, stream=None) ->
     _check(_lib.ttc_tt_svd(int(B), int(d.size), _ptr(d), _ptr(dense) if dense.numel() else None, _ptr(pm),
                            float(eps), _ptr(cores), _ptr(ranks), _ptr(ws) if ws is not None else None,
                            int(ws.numel()) if ws is not None else 0, _stream_handle(stream)))
+    _keep_alive(stream, dense.device, ws, cores, ranks)
     rdims = d if pm is None else d[pm - 1]
+    if B and torch.cuda.is_available():
+        _torch_stream(stream, dense.device).synchronize()   # the ranks are written by kernels on `stream`
     r = ranks[:B].cpu().numpy()
     return TTDevice(cores, rdims, ranks=r, offsets=np.arange(B, dtype=np.int64) * cap)
 

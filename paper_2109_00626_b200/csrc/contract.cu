@@ -374,4 +374,6 @@ cudaError_t launch_contract(const ContractArgs& a, size_t smem_bytes, cudaStream
     return cudaGetLastError();
 }
 
+cudaError_t contract_func_attributes(cudaFuncAttributes* fa) { return cudaFuncGetAttributes(fa, contract_kernel); }
+
 }  // namespace ttc

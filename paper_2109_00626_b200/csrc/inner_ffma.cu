@@ -17,9 +17,10 @@
 // Staging: the warp copies its own future steps into a private ring with 16-byte cp.async, inserting 4 floats
 // of padding after every contiguous run (F: runs of Fa, G: runs of Ga*I) so that the 8 (or 4) distinct runs
 // one LDS.128 touches fall into distinct bank groups; Z and W are kept with padded row strides likewise.
-// Pairs are handed out by a per-launch atomic ticket (dynamic load balance over heterogeneous pairs).
+// Pairs are assigned statically: warp w of W takes positions w, 2W-1-w, 2W+w, 4W-1-w, ... of the work list
+// (a "snake" over the cost-descending list of ttc_inner_ordered balances heterogeneous pairs); no global state,
+// so concurrent launches and graph replays on several streams are independent (re-entrant, ttc.h).
 #include <algorithm>
-#include <atomic>
 
 #include "tc_common.cuh"
 #include "ttc_internal.h"
@@ -29,7 +30,6 @@ namespace {
 
 constexpr int kPad = 4;
 constexpr int kQ = 4;                   // staged steps in flight per warp
-constexpr int kSlots = 1024;            // ticket counters (one per launch, reused round robin)
 
 constexpr int kMagicMax = 1024;          // exact-division table: q in [2, kMagicMax]
 
@@ -42,14 +42,10 @@ struct MagicTable {
 };
 __constant__ MagicTable c_magic = MagicTable();
 
-__device__ unsigned int g_ticket[kSlots];
-__device__ unsigned int g_done[kSlots];
-
 struct FfArgs {
     int ring;         // floats of one warp's ring
     int zbuf, wbuf;   // floats of the Z and W buffers
     int warp_floats;  // ring + Z + W + queue
-    int slot;         // ticket counter of this launch
 };
 
 struct FStep {
@@ -254,13 +250,15 @@ struct FCursor {
     int b, n, R, P;
     int64_t xo, yo;
     bool valid;
+    unsigned k;       // pairs taken so far by this warp
 };
 
-// Next pair from the launch's ticket counter; its rank rows go to rk (X: rk[0..N], Y: rk[N+1..2N+1]).
-__device__ __forceinline__ void fc_pop(const InnerArgs& a, const FfArgs& w, FCursor& c, int* rk, int lane) {
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(&g_ticket[w.slot], 1u);
-    t = __shfl_sync(0xffffffffu, t, 0);
+// This warp's next pair (static snake assignment over the work list); its rank rows go to rk (X: rk[0..N],
+// Y: rk[N+1..2N+1]).
+__device__ __forceinline__ void fc_pop(const InnerArgs& a, const FfArgs&, FCursor& c, int* rk, int lane) {
+    const unsigned W = gridDim.x, w = blockIdx.x;
+    const unsigned t = c.k * W + ((c.k & 1u) ? W - 1u - w : w);
+    ++c.k;
     c.valid = t < (unsigned)a.B;
     if (!c.valid) return;
     c.b = a.order ? __ldg(a.order + t) : (int)t;
@@ -289,6 +287,7 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
     int* rk = reinterpret_cast<int*>(q + kQ);
     const int N = a.N;
     FCursor ic;
+    ic.k = 0;
     fc_pop(a, w, ic, rk, lane);
     unsigned head = 0, tail = 0, head_off = 0;
     int qh = 0, qn = 0;
@@ -371,16 +370,6 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
         --qn;
     }
     tc::cp_wait_pending(0);
-    // the last warp of the launch resets its ticket slot for a later launch
-    if (lane == 0) {
-        __threadfence();
-        const unsigned total = gridDim.x;
-        if (atomicAdd(&g_done[w.slot], 1u) == total - 1) {
-            g_ticket[w.slot] = 0;
-            g_done[w.slot] = 0;
-            __threadfence();
-        }
-    }
 }
 
 // Floats of the per-warp buffers for a batch whose interior ranks are <= max_rank and dims <= max_dim.
@@ -397,8 +386,6 @@ FfSizes ffma_sizes(int max_rank, int max_dim, int N) {
     return z;
 }
 constexpr int64_t kSmemPerSM = 228 * 1024, kSmemPerCTA = 227 * 1024, kReservedPerCTA = 1024;
-
-std::atomic<unsigned> g_launches{0};
 
 }  // namespace
 
@@ -429,7 +416,6 @@ cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s) 
     w.wbuf = (int)z.wbuf;
     w.ring = (int)((warp_floats - fixed) & ~int64_t(3));
     w.warp_floats = (int)(w.ring + fixed);
-    w.slot = (int)(g_launches.fetch_add(1) % kSlots);
     const size_t smem = sizeof(float) * (size_t)w.warp_floats;
     cudaError_t e = cudaFuncSetAttribute(inner_ffma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

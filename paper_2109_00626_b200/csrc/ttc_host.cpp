@@ -116,6 +116,9 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
     if (!t->offsets_host && !h->uniform && t->batch > 1)
         return fail(TTC_ERR_ARG, "%s: heterogeneous ranks need explicit offsets", name);
     if (t->batch > 0 && !t->cores) return fail(TTC_ERR_NULL, "%s: cores is NULL", name);
+    if (t->batch > 0 && t->n_elems < 1)
+        return fail(TTC_ERR_ARG, "%s: n_elems = %lld: the number of floats at cores is required (>= 1)", name,
+                    (long long)t->n_elems);
     if (t->cores && (reinterpret_cast<uintptr_t>(t->cores) & 3u))
         return fail(TTC_ERR_ALIGN, "%s: cores pointer not 4-byte aligned", name);
     // sizes and bounds, overflow-checked.  A train has at most TTC_MAX_ORDER cores of at most
@@ -130,7 +133,7 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
     if (!t->offsets_host && h->uniform && t->batch > 0) {   // packed uniform: the last train bounds everything
         int64_t last;
         if (!mul_ok(h->train_elems_uniform, t->batch, &last)) return fail(TTC_ERR_OVERFLOW, "%s: batch size overflows", name);
-        if (t->n_elems > 0 && last > t->n_elems)
+        if (last > t->n_elems)
             return fail(TTC_ERR_OVERFLOW, "%s: %d packed trains of %lld floats exceed n_elems = %lld", name,
                         t->batch, (long long)h->train_elems_uniform, (long long)t->n_elems);
         return TTC_OK;
@@ -140,7 +143,7 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
         int64_t start = t->offsets_host ? t->offsets_host[b] : packed_end, end;
         if (start < 0) return fail(TTC_ERR_OVERFLOW, "%s pair %d: offset %lld < 0", name, b, (long long)start);
         if (!add_ok(start, elems, &end)) return fail(TTC_ERR_OVERFLOW, "%s pair %d: offset + size overflows", name, b);
-        if (t->n_elems > 0 && end > t->n_elems)
+        if (end > t->n_elems)
             return fail(TTC_ERR_OVERFLOW, "%s pair %d: train [%lld, %lld) runs past n_elems = %lld", name, b,
                         (long long)start, (long long)end, (long long)t->n_elems);
         packed_end = end;
@@ -247,8 +250,8 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
     const bool uniform = hx.uniform && hy.uniform && hx.urank == hy.urank;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    // TTC_KERNEL=generic|fast|wpp|small forces the general-shape / CTA-per-pair / warp-per-pair tensor-core /
-    // tiny-batch kernel (cross-checks)
+    // TTC_KERNEL=generic|fast|small|ffma forces the general-shape / CTA-per-pair tensor-core / tiny-batch /
+    // warp-per-pair FP32 kernel (cross-checks and A/B measurements)
     const char* kv = std::getenv("TTC_KERNEL");
     const bool force_generic = kv && std::strcmp(kv, "generic") == 0;
     // uniform rank-16 trains with 16-byte aligned cores and trains: the specialised rank-16 kernel
@@ -259,7 +262,7 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
     }
     const bool uniform_r16 = uniform && hx.urank == 16 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     const bool force_fast = kv && std::strcmp(kv, "fast") == 0;
-    const bool force_wpp = kv && std::strcmp(kv, "wpp") == 0;
+    const bool force_ffma = kv && std::strcmp(kv, "ffma") == 0;
     const bool uniform_r64 = uniform && hx.urank == 64 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     // tiny batches are latency-bound: both trains of a pair staged at once, one DRAM round trip per pair
     // (TTC_KERNEL=small forces it for any batch that fits, for cross-checks)
@@ -287,14 +290,15 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
             return TTC_OK;
         }
     }
-    if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
+    const bool ffma_ok = ttc::inner_ffma_supported(a, mr, hx.mult8 && hy.mult8);
+    if (force_ffma && ffma_ok)
+        e = ttc::launch_inner_ffma(a, mr, s);
+    else if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
         e = ttc::launch_inner_r16(a, s);
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
         e = ttc::launch_inner_r64(a, s);
-    else if (!force_generic && !force_fast && !force_wpp && ttc::inner_ffma_supported(a, mr, hx.mult8 && hy.mult8))
+    else if (!force_generic && !force_fast && ffma_ok)
         e = ttc::launch_inner_ffma(a, mr, s);   // warp per pair on the FP32 pipe (ranks multiple of 8, <= 32)
-    else if (!force_generic && !force_fast && force_wpp && ttc::inner_wpp_supported(a, mr))
-        e = ttc::launch_inner_wpp(a, mr, hx.mult8 && hy.mult8, s);   // warp per pair (ranks multiple of 8: full tiles)
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);
     else
@@ -419,7 +423,9 @@ ttc_status ttsvd_shape(int32_t order, const int32_t* dims, const int32_t* perm, 
         (*stride)[k] = xs[m - 1];
     }
     int64_t total = 1;
-    for (int k = 0; k < order; ++k) total *= (*rd)[k];
+    for (int k = 0; k < order; ++k)
+        if (!mul_ok(total, (*rd)[k], &total) || total > (int64_t(1) << 40))
+            return fail(TTC_ERR_OVERFLOW, "dense size overflows");
     // capacity: R_n <= min(prod_{k<=n} I_k, prod_{k>n} I_k); the Gram side of step n <= min(R_{n-1} I_n, rest)
     int64_t c = 0, left = 1, g = 1;
     int64_t Rprev = 1;
@@ -996,6 +1002,16 @@ ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const
     }
     a.stage_off = (int32_t)p->scratch_floats;
     a.stage_floats = max_train <= 10240 ? (int32_t)max_train : 0;
+    {   // stage only when transfer scratch + staged trains + the kernel's static shared memory fit one block
+        int dev = 0, optin = 0;
+        cudaFuncAttributes fa;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+        if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+            return cuda_fail(e, "cudaDeviceGetAttribute");
+        if ((e = ttc::contract_func_attributes(&fa)) != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+        const int64_t need = 4 * (p->scratch_floats + a.stage_floats) + (int64_t)fa.sharedSizeBytes;
+        if (need > optin) a.stage_floats = 0;
+    }
     e = ttc::launch_contract(a, sizeof(float) * ((size_t)p->scratch_floats + (size_t)a.stage_floats), s);
     if (e != cudaSuccess) return cuda_fail(e, "ttc_contract launch");
     return TTC_OK;

@@ -34,8 +34,6 @@ cudaError_t launch_inner_fast(const InnerArgs& a, int max_rank, bool uniform, cu
 bool        inner_r16_supported(const InnerArgs& a, bool uniform_r16);
 cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s);
 bool        inner_r64_supported(const InnerArgs& a, bool uniform_r64);
-bool        inner_wpp_supported(const InnerArgs& a, int max_rank);
-cudaError_t launch_inner_wpp(const InnerArgs& a, int max_rank, bool ranks_mult8, cudaStream_t s);
 cudaError_t launch_inner_r64(const InnerArgs& a, cudaStream_t s);
 // tiny batches (inner_small.cu): both trains of a pair in SMEM at once; floats of each region
 struct SmallLayout {
@@ -83,6 +81,7 @@ struct ContractArgs {
 };
 
 cudaError_t launch_contract(const ContractArgs& a, size_t smem_bytes, cudaStream_t s);
+cudaError_t contract_func_attributes(cudaFuncAttributes* fa);   // static shared memory of the contract kernel
 
 // ---- TTCP splice of end modes (splice.cu) ------------------------------------------------------------
 struct SpliceArgs {

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import TTDevice, ttc_inner, ttc_pair_cost, ttc_partition
+from . import TTDevice, _keep_alive, ttc_inner, ttc_pair_cost, ttc_partition
 
 
 def shard_bounds(cost: Sequence[float], world: int) -> np.ndarray:
@@ -59,7 +59,11 @@ def sharded_inner(x: TTDevice, y: TTDevice, group=None, gather: bool = True, cos
         cost, _ = ttc_pair_cost(x, y)
     bounds = shard_bounds(cost, world)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-    out = ttc_inner(shard_view(x, lo, hi), shard_view(y, lo, hi), stream=stream)
+    xs, ys = shard_view(x, lo, hi), shard_view(y, lo, hi)
+    out = ttc_inner(xs, ys, stream=stream)
+    # the shard views' device rank / offset tables are freed when this function returns, possibly while the
+    # kernel on `stream` still reads them: hand them to the caching allocator's stream tracking
+    _keep_alive(stream, x.cores.device, xs.ranks_dev, xs.offsets_dev, ys.ranks_dev, ys.offsets_dev)
     if not gather:
         return out, bounds
     return gather_results(out, bounds, group), bounds

@@ -22,3 +22,13 @@ def tcp(x, y, x_modes, y_modes):
 
 def random_train(rng, dims, ranks, scale=1.0):
     return [rng.standard_normal((ranks[n], dims[n], ranks[n + 1])) * scale for n in range(len(dims))]
+
+
+def tensor_with_unfolding_spectrum(rng, dims, s):
+    """A dense tensor (Eq. 2 order) whose mode-1 unfolding X_(1) (I_1 x prod_{k>1} I_k) has exactly the singular
+    values s: X_(1) = U diag(s) V^T with U, V orthonormal columns from QR of Gaussian matrices."""
+    s = np.asarray(s, dtype=np.float64)
+    m, n = dims[0], int(np.prod(dims[1:]))
+    U, _ = np.linalg.qr(rng.standard_normal((m, s.size)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, s.size)))
+    return (U @ np.diag(s) @ V.T).reshape(dims, order="F")

@@ -324,3 +324,24 @@ def test_every_compute_entry_is_a_noop_on_an_empty_batch():
                           None) == ttc.TTC_OK
     nb = ctypes.c_int64(-1)
     assert lib.ttc_tt_svd_workspace(0, 3, ttc._ptr(dims), None, ctypes.byref(nb)) == ttc.TTC_OK and nb.value == 0
+
+
+def test_n_elems_is_required_and_bounds_every_train():
+    """ttc.h: n_elems >= 1 is required when batch > 0 (TTC_ERR_ARG, no unchecked device reads); a packed uniform
+    batch or an offset train running past n_elems is TTC_ERR_OVERFLOW."""
+    x, y = _dev(), _dev()
+    x.c.n_elems = 0
+    assert _call_inner(x, y) == ttc.TTC_ERR_ARG
+    assert "n_elems" in ttc.ttc_last_error()
+    x, y = _dev(), _dev()
+    x.c.n_elems -= 1
+    assert _call_inner(x, y) == ttc.TTC_ERR_OVERFLOW
+
+
+def test_tt_svd_dense_size_overflow_is_detected():
+    """The dense size prod I_n is overflow-checked before use ({2^20, 2^20, 2^24} used to wrap to 0)."""
+    cap = ctypes.c_int64(0)
+    d = np.array([1 << 20, 1 << 20, 1 << 24], np.int32)
+    assert ttc._lib.ttc_tt_svd_capacity(3, d.ctypes.data, None, ctypes.byref(cap)) == ttc.TTC_ERR_OVERFLOW
+    d = np.array([1 << 15, 1 << 15, 1 << 15], np.int32)   # 2^45 > 2^40
+    assert ttc._lib.ttc_tt_svd_capacity(3, d.ctypes.data, None, ctypes.byref(cap)) == ttc.TTC_ERR_OVERFLOW

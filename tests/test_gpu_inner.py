@@ -73,20 +73,49 @@ def test_c2_full_size_sampled():
     _check(Xs, Ys, got, _sample(Xs.B, 16, 1), "self")
 
 
-def test_c4_sampled():
-    """BASELINE.json configs[3] (R=64) in the bench's launch configuration (one 1,024-pair shard of 8,192),
-    sampled pairs vs the oracle; and 512 self pairs (non-vacuous control)."""
-    for kind, B in (("iid", 1024), ("self", 512)):
+def _run_sentinel(X, Y, order=False):
+    """ttc_inner into a NaN-filled output on the device: every pair must be written (finite afterwards)."""
+    XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+    out = torch.full((X.B,), float("nan"), dtype=torch.float32, device=DEV)
+    ttc.ttc_inner(XD, YD, out=out, order=ttc.ttc_cost_order(XD, YD) if order else None)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.float64)
+    assert np.all(np.isfinite(got)), f"{int(np.sum(~np.isfinite(got)))} of {X.B} pairs never written"
+    return got, XD, YD
+
+
+@pytest.mark.parametrize("B", [8192])
+def test_c4_full_batch(B):
+    """BASELINE.json configs[3] (R = 64) at its full single-GPU batch (8,192 pairs), the bench's launch: iid pairs
+    and the non-vacuous self / correlated controls, 64 sampled pairs each (first and last pair included)."""
+    for kind, k in (("self", 64), ("corr", 64), ("iid", 16)):
         X, Y = ttgen.config_batch("C4", kind=kind, B=B, device=DEV)
-        got = _run(X, Y)
-        _check(X, Y, got, _sample(X.B, 8), kind)
+        got, _, _ = _run_sentinel(X, Y)
+        _check(X, Y, got, _sample(X.B, k, 7), kind)
+        del X, Y
+        torch.cuda.empty_cache()
 
 
-def test_c5_sampled():
-    """BASELINE.json configs[4] (heterogeneous ranks {8..32}, N=64, I=2): one 8-GPU shard (8192 pairs)."""
-    X, Y = ttgen.config_batch("C5", kind="iid", B=8192, device=DEV)
-    got = _run(X, Y)
-    _check(X, Y, got, _sample(X.B, 16), "iid")
+@pytest.mark.parametrize("B,kinds", [(8192, ("self", "corr", "iid")), (65536, ("corr",))])
+def test_c5_full_batch(B, kinds):
+    """BASELINE.json configs[4] (ranks {8..32}, N = 64, I = 2) at one 8-GPU shard (8,192 pairs) and at the full
+    65,536-pair batch on one GPU, with the cost-descending work list the bench uses (ttc_inner_ordered): the
+    first and last tickets (the most and least expensive pairs) and the first / last pair indices are among
+    >= 64 sampled pairs on non-vacuous self / correlated batches; the ordered and natural-order launches agree
+    bitwise on every pair; a NaN sentinel shows that every pair was written."""
+    for kind in kinds:
+        X, Y = ttgen.config_batch("C5", kind=kind, B=B, device=DEV)
+        got, XD, YD = _run_sentinel(X, Y, order=True)
+        order = ttc.ttc_cost_order(XD, YD).host
+        idx = sorted(set(_sample(X.B, 64, 3)) | {int(order[0]), int(order[1]), int(order[-2]), int(order[-1])})
+        _check(X, Y, got, idx, kind)
+        nat, _, _ = _run_sentinel(X, Y, order=False)
+        assert np.array_equal(nat.view(np.uint64), got.view(np.uint64))
+        del X, Y, XD, YD
+        torch.cuda.empty_cache()
+
+
+def test_c5_small_corr():
     X, Y = ttgen.config_batch("C5", kind="corr", B=256, device=DEV)
     got = _run(X, Y)
     _check(X, Y, got, _sample(X.B, 16, 2), "corr")
@@ -199,9 +228,9 @@ def test_uniform_rank16_shapes(dims):
     _check(X, X, got, range(B), "self")
 
 
-@pytest.mark.parametrize("variant", ["generic", "fast", "wpp", "small"])
+@pytest.mark.parametrize("variant", ["generic", "fast", "ffma", "small"])
 def test_kernel_variants_agree(monkeypatch, variant):
-    """Every tt_inner kernel (default dispatch vs TTC_KERNEL=generic / fast / wpp) agrees within fp32 rounding."""
+    """Every tt_inner kernel (default dispatch vs TTC_KERNEL=generic / fast / ffma / small) agrees within fp32 rounding."""
     for cfg, B in (("C2", 16), ("C5", 24), ("C1", 1), ("C4", 2)):
         X, Y = ttgen.config_batch(cfg, kind="corr", B=B)
         ref = _run(X, Y)

@@ -143,3 +143,20 @@ def test_pipeline_matches_fused_kernel(dims, eps, monkeypatch):
             assert np.max(np.abs(p - f)) <= 1e-4 * max(1.0, scale), f"tensor {b}: cores differ"
         err = np.linalg.norm(ref.dense_from_tt(cp) - Xs[b]) / scale
         assert err <= max(eps, 2e-5) * (1 + 1e-4)
+
+
+@pytest.mark.parametrize("spectrum,want", [((1.0, 1e-5, 1e-9), 2), ((1.0, 3e-7, 3e-8), 2), ((1.0, 0.5, 2e-7), 3)])
+def test_sigma_floor_on_constructed_spectra(spectrum, want):
+    """R25 on the GPU: first-unfolding singular values straddling the 1e-7 sigma_max floor (tests/
+    test_oracle_ttsvd.py pins the oracle on the same tensors).  A Gram eigenproblem solved in fp32, or a floor
+    other than the oracle's, would drop 1e-5 / 3e-7 / 2e-7 or keep 1e-9 / 3e-8 and fail the rank check."""
+    rng = np.random.default_rng(int(1e3 * spectrum[1]) + len(spectrum))
+    X = ref.tensor_with_unfolding_spectrum(rng, (20, 20, 20), spectrum)
+    X32 = X.astype(np.float32).astype(np.float64)
+    T = ttc.ttc_tt_svd(_dense_batch([X32, X32]), (20, 20, 20), 0.0)
+    want_cores = ttsvd.tt_svd(X32, 0.0)
+    assert want_cores[0].shape[2] == want
+    for cs in _trains(T):
+        assert [c.shape for c in cs] == [c.shape for c in want_cores]
+        err = np.linalg.norm(ref.dense_from_tt(cs) - X32) / np.linalg.norm(X32)
+        assert err <= 2e-5

@@ -87,9 +87,14 @@ def test_k_step_count_pins(I, R, want):
     X, Y = ref.random_train(rng, dims, ranks), ref.random_train(rng, dims, ranks)
     res = oracle.tt_contract(X, Y, [1], [1])
     assert res["t_macs"] == want
-    # and the transfer is Eq. 12's K: absorbed into the next core (X_2 (x) I) it gives the Z^rho train
-    K_mat = X[0][0].T @ Y[0][0]
+    # and the transfer is Eq. 12's K = A_x^T A_y (R_1 x P_1): absorbed into the next core (X_2 (x) I_{P_1}),
+    # core 1 of the output is sum_r K[r, p] X_2[r, i, r'] at bond index r' + R_2 p (R9, R10)
     assert res["order"] == 8
+    K_mat = X[0][0].T @ Y[0][0]
+    X2 = X[1]
+    R2 = X2.shape[2]
+    want = np.einsum("rp,ris->isp", K_mat, X2).reshape(1, dims[1], R2 * R, order="F")
+    np.testing.assert_allclose(res["cores"][0], want, rtol=1e-12, atol=1e-12 * np.max(np.abs(want)))
 
 
 def test_single_leading_pair_transfer_is_eq12():
@@ -161,3 +166,33 @@ def test_mode_errors():
         oracle.tt_contract(X, Y, [1, 2], [2, 1])   # crossing pairs are not a ladder
     with pytest.raises(oracle.OracleError):
         oracle.tt_contract(X, Y, [1], [1])         # I_1 = 2 != J_1 = 3
+
+
+def test_batch_wrappers_equal_single_pair_calls():
+    """oracle_tt_contract_batch / oracle_tt_splice_batch (the C3 / S1 cpu_baseline legs) return, pair by pair at
+    the caller's offsets, exactly what the single-pair O3 / O5 return (same loops, so bitwise), including a
+    sub-range (first, count) and more threads than pairs."""
+    for cfg in ("C3", "S1"):
+        c = ttgen.CONFIGS[cfg]
+        B = 5
+        X, Y = ttgen.config_batch(cfg, B=B)
+        singles = []
+        for b in range(B):
+            if cfg == "C3":
+                singles.append(oracle.tt_contract(X.train(b), Y.train(b), list(c["x_modes"]), list(c["y_modes"])))
+            else:
+                singles.append(oracle.tt_splice(X.train(b), Y.train(b), c["x_mode"], c["y_mode"]))
+        per = singles[0]["elems"]
+        for first, count, nth in ((0, B, 1), (0, B, 8), (2, 3, 2)):
+            gap = 7   # non-packed output layout: trains 7 floats apart, in reverse order
+            offs = np.array([(count - 1 - j) * (per + gap) for j in range(count)], np.int64)
+            total = count * (per + gap)
+            if cfg == "C3":
+                out = oracle.tt_contract_batch(X, Y, list(c["x_modes"]), list(c["y_modes"]), offs, total, nth, first,
+                                               count)
+            else:
+                out = oracle.tt_splice_batch(X, Y, c["x_mode"], c["y_mode"], offs, total, nth, first, count)
+            for j in range(count):
+                seg = out[offs[j]: offs[j] + per]
+                assert np.array_equal(seg, singles[first + j]["flat"]), (cfg, first, j)
+                assert not np.any(out[offs[j] + per: offs[j] + per + gap])   # nothing written in the gaps

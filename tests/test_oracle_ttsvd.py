@@ -82,3 +82,35 @@ def test_alg2_equals_eq8(shape_x, shape_y, n, m):
     for eps in (0.1, 0.3):
         got = ttsvd.ttcp_dense(X, Y, n, m, eps)
         assert np.linalg.norm(got - want) <= (2 * eps + eps ** 2) * np.linalg.norm(X) * np.linalg.norm(Y)
+
+
+@pytest.mark.parametrize("spectrum,want", [((1.0, 1e-5, 1e-9), 2), ((1.0, 3e-7, 3e-8), 2), ((1.0, 0.5, 2e-7), 3)])
+def test_sigma_floor_on_constructed_spectra(spectrum, want):
+    """R25 pinned on spectra that straddle the floor: singular values of the first unfolding above 1e-7 sigma_max
+    are kept at eps = 0 (1e-5, 3e-7, 2e-7), those below it are dropped (1e-9, 3e-8) -- on the fp64 tensor and on
+    its fp32 rounding (what a GPU caller passes: the rounding adds singular values near 1e-8, below the floor).
+    The kept part reconstructs the tensor to the dropped singular value (Eckart-Young: ||X - X_R|| = s_R)."""
+    rng = np.random.default_rng(int(1e3 * spectrum[1]) + len(spectrum))
+    X = ref.tensor_with_unfolding_spectrum(rng, (20, 20, 20), spectrum)
+    s = np.linalg.svd(X.reshape(20, -1, order="F"), compute_uv=False)
+    np.testing.assert_allclose(s[:3], spectrum, rtol=1e-6, atol=1e-15)
+    for Xin in (X, X.astype(np.float32).astype(np.float64)):
+        cores = ttsvd.tt_svd(Xin, 0.0)
+        assert cores[0].shape[2] == want
+        dropped = spectrum[want] if want < len(spectrum) else 0.0
+        err = np.linalg.norm(_dense(cores) - Xin)
+        assert err <= dropped + 1e-7 * np.linalg.norm(Xin)
+
+
+def test_sigma_floor_is_fp32_input_resolution():
+    """R25's floor is the resolution of fp32 input data: rounding a tensor to fp32 moves its singular values by at
+    most ||X - fl32(X)||_2 <= ||X - fl32(X)||_F <= 2^-24 ||X||_F (Weyl), and for a rank-1 unfolding sigma_max =
+    ||X||_F, so 2^-24 = 6e-8 < 1e-7: spurious singular values created by the rounding never pass the floor."""
+    rng = np.random.default_rng(9)
+    for dims in ((20, 20, 20), (8, 50, 20), (40, 10, 20)):
+        X = ref.tensor_with_unfolding_spectrum(rng, dims, (1.0,))
+        X32 = X.astype(np.float32).astype(np.float64)
+        assert np.linalg.norm(X - X32) <= 2.0 ** -24 * np.linalg.norm(X)
+        s = np.linalg.svd(X32.reshape(dims[0], -1, order="F"), compute_uv=False)
+        assert s[1] < ttsvd.SIGMA_FLOOR * s[0]
+        assert [c.shape[2] for c in ttsvd.tt_svd(X32, 0.0)[:1]] == [1]
