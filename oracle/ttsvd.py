@@ -13,9 +13,10 @@ Alg. 1, step by step in the paper's order and notation:
 Readings: "USV" is U S V^T (R22); R_n is the SMALLEST rank whose discarded singular values satisfy
 sum_{j > R_n} s_j^2 <= delta^2 (R23); singular vectors carry a sign convention -- the entry of largest magnitude
 of every column of U is positive, the corresponding row of S V^T flipped with it (R24: the TT-SVD is unique only
-up to these signs); singular values at or below 1e-7 of the largest count as zero (R25: the resolution of a
-singular value obtained through an fp64 Gram eigenproblem, which is how the GPU computes them), so eps = 0
-returns the numerical TT ranks.
+up to these signs); singular values at or below 1e-7 of the largest count as zero (R25: the resolution of the
+input data -- operands arrive in fp32, and rounding a tensor to fp32 moves its singular values by up to
+||X - fl32(X)||_2 <= 2^-24 ||X||_F ~ 6e-8 ||X||_F (Weyl), so smaller ones are not determined by the input; pinned on
+constructed spectra in tests/test_oracle_ttsvd.py), so eps = 0 returns the numerical TT ranks.
 """
 import numpy as np
 
