@@ -1,0 +1,598 @@
+// inner_r64tc.cu -- tt_inner for uniform rank-64 trains with mode sizes I_n = 4 (BASELINE.json C4: N = 16, I = 4,
+// R = 64, "the tensor-core path") on the 5th-generation tensor cores: tcgen05.mma kind::tf32 with the
+// accumulators in tensor memory, operands staged by TMA (cp.async.bulk.tensor) in the 128-byte-swizzled K-major
+// layout the MMA reads.  Same sweep as ttc.h:
+//   Z_0 = [1],  Z_n = sum_i X_n[:, i, :]^T Z_{n-1} Y_n[:, i, :]  (Fig. 1b / Eq. 12 chained),  out = Z_N.
+//
+// Interior step n, in two GEMM families (Eq. 2 layout: Y_n[p, i, q] at p + 64 i + 256 q, X_n[r, i, s] likewise):
+//   GEMM-1, per half h (slices i = 2h, 2h+1), M = 128:
+//       D1_h[m = i' + 2q][r] = sum_p Y_n[p, 2h+i', q] Z[r][p]          (= W_i[r][q], W_i = Z Y_n[:, i, :])
+//       A = the Y_n slice pair as 128 rows x 64 p (a 3-D TMA box: p fastest, then i', then q), B = Z (64 r x 64 p)
+//   GEMM-2, per slice i, M = 64:
+//       D2[s][q] += sum_r X_n[r, i, s] W_i[r][q]                        (= Z_n after the four slices)
+//       A = X_n[:, i, :]^T as 64 rows s x 64 r (2-D TMA boxes), B = W_i (64 q x 64 r, written by threads)
+// 3xTF32: an input core value x (TMA-staged) is fed as its raw bits (the tensor core truncates them to tf32 --
+// measured, tools/tc05_probe.cu) and as lo = RN_tf32(x - trunc_tf32(x)); the operands the threads write (Z, W)
+// as hi = RN_tf32(x) and lo = x - hi; a.b ~ a_hi b_hi + a_lo b_hi + a_hi b_lo with every dropped or rounded term of
+// random sign.  Accumulation stays in TMEM over the whole K (measured as accurate as
+// sequential fp32 round-to-nearest, tools/tc05_probe.cu).
+//
+// Warp roles (one persistent CTA per SM, pairs assigned statically):
+//   warp 0  TMA producer: 8 tiles of 16 KB per step into a 4-slot ring (+ the pair's boundary cores, 4 KB)
+//   warp 1  TMEM allocator and MMA issuer (one thread)
+//   warps 2-5 epilogue warps (one per TMEM sub-partition): the D1 -> W (hi, lo) and D2 -> Z (hi, lo)
+//            epilogues through tcgen05.ld (partial accumulators summed in fp32), the boundary steps
+//            (Z_1 = A_x^T A_y, Eq. 12, and the final scalar) on the FP32 pipe
+//   warps 6-7 lo workers: the lo parts of the staged input tiles (3-buffer ring)
+#include <cuda.h>
+
+#include "tc_common.cuh"
+#include "ttc_internal.h"
+
+namespace ttc {
+namespace {
+
+using namespace tc;
+
+constexpr int kTile = 16384;                      // bytes of one staged tile
+constexpr int kRaw = 4, kLo = 3;                  // ring depths (raw input tiles / their lo parts)
+constexpr int kThreads = 256;                   // 8 warps (see the roles below): 2 per SM sub-partition
+constexpr int kTilesPerStep = 8;                  // Y halves (2 K-chunks each), then X slices 0..3
+
+// shared-memory layout (bytes from the 1024-aligned base)
+constexpr int kOffRaw = 0;
+constexpr int kOffLo = kOffRaw + kRaw * kTile;
+constexpr int kOffB2 = kOffLo + kLo * kTile;      // 2 buffers x {raw 16 KB, lo 16 KB}: W_i as the GEMM-2 B operand
+constexpr int kOffB1 = kOffB2 + 4 * kTile;        // {raw 16 KB, lo 16 KB}: Z as the GEMM-1 B operand
+constexpr int kOffBnd = kOffB1 + 2 * kTile;       // 2 buffers x {X_1, Y_1, X_N, Y_N} x 1 KB
+constexpr int kOffRed = kOffBnd + 2 * 4096;       // 4 floats: the final reduction
+constexpr int kOffBar = kOffRed + 64;
+constexpr int kNumBars = 32;
+constexpr int kSmemBytes = kOffBar + 8 * kNumBars + 16 + 1024;   // + TMEM address slot + alignment slack
+
+// barrier indices
+constexpr int FULL = 0, EMPTY = 4, LO_READY = 8, LO_FREE = 11, D1_FULL = 14, D1_EMPTY = 16, B2_READY = 18,
+              B2_FREE = 20, D2_FULL = 22, B1_READY = 23, BND_FULL = 24, BND_EMPTY = 26, D2P_FULL = 28, D2P_EMPTY = 30;
+
+// TMEM columns (512 allocated).  The tensor core's accumulation into TMEM truncates (measured: -5.6e-8 relative per
+// accumulating MMA on positive sums, tools/tc05_probe.cu), so long chains are split: the large a_hi b_hi products
+// accumulate in short chains -- GEMM-1 8 MMAs per half, GEMM-2 4 per (slice, K-chunk) -- and the small cross terms
+// (2^-11 smaller, their truncation negligible) in separate accumulators; the converters add the partials in fp32
+// round-to-nearest.
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kD1M = 0;      // + 64 h: GEMM-1 a_hi b_hi, half h (M = 128)
+constexpr uint32_t kD1L = 128;    // + 64 h: GEMM-1 cross terms
+constexpr uint32_t kD2P = 256;    // + 64 (i & 1): GEMM-2 a_hi b_hi of slice i, K-chunk kc at lanes 16 kc + (0..15)
+constexpr uint32_t kD2L = 384;    // GEMM-2 cross terms of all four slices (M = 64: lanes 0..15)
+
+struct TcArgs {
+    int32_t B, N;
+    int64_t pair_elems;       // floats per train (packed)
+    const float* x;
+    const float* y;
+    float* out;
+    const int32_t* order;
+};
+
+__device__ __forceinline__ uint64_t* bar_at(unsigned char* base, int i) {
+    return reinterpret_cast<uint64_t*>(base + kOffBar) + i;
+}
+
+// ---- tcgen05 / TMA wrappers -----------------------------------------------------------------------------
+// K-major SWIZZLE_128B operand descriptor (rows of 128 B, 8-row groups 1024 B apart), sm_100 version bit
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dt), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// 32 consecutive TMEM columns of this warp's 32 lanes (thread t <-> lane t of the warp's sub-partition)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                   "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                   "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                   "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// lo part of a 3xTF32 split: x - trunc_tf32(x) (exact), rounded to nearest tf32 (so the tensor core's own
+// truncation of it is exact and the remaining error has a random sign)
+__device__ __forceinline__ float lo_rn(float x) {
+    const float l = x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+    return __uint_as_float((__float_as_uint(l) + 0x1000u) & 0xffffe000u);
+}
+__device__ __forceinline__ float4 lo_rn4(float4 v) { return make_float4(lo_rn(v.x), lo_rn(v.y), lo_rn(v.z), lo_rn(v.w)); }
+// split of the operands the threads write (Z, W): hi = RN_tf32(x), lo = x - hi (exact; the tensor core truncates
+// it).  lo has a random sign, so the dropped lo_a lo_b term and lo's truncation are unbiased (a truncation split
+// on both sides biases every product by ~2^-22 |ab| and drifted 6e-5 over C4's 14 steps on self pairs).
+__device__ __forceinline__ void split_rn4(float4 v, float4& hi, float4& lo) {
+    hi.x = __uint_as_float((__float_as_uint(v.x) + 0x1000u) & 0xffffe000u);
+    hi.y = __uint_as_float((__float_as_uint(v.y) + 0x1000u) & 0xffffe000u);
+    hi.z = __uint_as_float((__float_as_uint(v.z) + 0x1000u) & 0xffffe000u);
+    hi.w = __uint_as_float((__float_as_uint(v.w) + 0x1000u) & 0xffffe000u);
+    lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+}
+
+// byte offset of element (row, k) in a K-major 128B-swizzled operand of 64-element rows stored as two 32-element
+// chunks of `rows` x 128 B each
+__device__ __forceinline__ uint32_t sw_off(int row, int k, int rows) {
+    return (uint32_t)((k >> 5) * rows * 128 + row * 128 + ((((k >> 2) & 7) ^ (row & 7)) << 4) + ((k & 3) << 2));
+}
+
+// one converter thread writes 64 values (row `row` of a 64-row operand, K = 0..63) as raw + lo
+__device__ __forceinline__ void write_row64(unsigned char* raw, unsigned char* lo, int row, const uint32_t (&v0)[32],
+                                            const uint32_t (&v1)[32]) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        const uint32_t* src = c < 8 ? v0 : v1;
+        const int j = (c & 7) * 4;
+        float4 f = make_float4(__uint_as_float(src[j]), __uint_as_float(src[j + 1]), __uint_as_float(src[j + 2]),
+                               __uint_as_float(src[j + 3]));
+        const uint32_t off = sw_off(row, 4 * c, 64);
+        float4 h, l;
+        split_rn4(f, h, l);
+        *reinterpret_cast<float4*>(raw + off) = h;
+        *reinterpret_cast<float4*>(lo + off) = l;
+    }
+}
+
+struct Cursor {       // the static pair sequence of this CTA
+    int it, b;
+    bool valid;
+};
+__device__ __forceinline__ void pair_at(const TcArgs& a, int it, Cursor& c) {
+    const int idx = blockIdx.x + it * gridDim.x;
+    c.it = it;
+    c.valid = idx < a.B;
+    c.b = c.valid ? (a.order ? __ldg(a.order + idx) : idx) : 0;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays a shared pointer
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + kOffBar + 8 * kNumBars);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int N = a.N;
+    const int steps = N - 2;                      // interior steps per pair
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) { mbar_init(bar_at(sm, FULL + i), 1); mbar_init(bar_at(sm, EMPTY + i), 1); }
+        for (int i = 0; i < 3; ++i) { mbar_init(bar_at(sm, LO_READY + i), 2); mbar_init(bar_at(sm, LO_FREE + i), 1); }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar_at(sm, D2P_FULL + i), 1); mbar_init(bar_at(sm, D2P_EMPTY + i), 4);
+            mbar_init(bar_at(sm, D1_FULL + i), 1); mbar_init(bar_at(sm, D1_EMPTY + i), 4);
+            mbar_init(bar_at(sm, B2_READY + i), 4); mbar_init(bar_at(sm, B2_FREE + i), 1);
+            mbar_init(bar_at(sm, BND_FULL + i), 1); mbar_init(bar_at(sm, BND_EMPTY + i), 4);
+        }
+        mbar_init(bar_at(sm, D2_FULL), 1);
+        mbar_init(bar_at(sm, B1_READY), 4);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(tslot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        // ================================================================ TMA producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
+            uint32_t k = 0;
+            Cursor c;
+            for (int it = 0;; ++it) {
+                pair_at(a, it, c);
+                if (!c.valid) break;
+                const int j = it & 1;
+                mbar_wait(bar_at(sm, BND_EMPTY + j), ((it >> 1) & 1) ^ 1);
+                unsigned char* bnd = sm + kOffBnd + j * 4096;
+                const float* xb = a.x + (int64_t)c.b * a.pair_elems;
+                const float* yb = a.y + (int64_t)c.b * a.pair_elems;
+                mbar_arrive_expect_tx(bar_at(sm, BND_FULL + j), 4096);
+                bulk_g2s(bnd, xb, 1024, bar_at(sm, BND_FULL + j));
+                bulk_g2s(bnd + 1024, yb, 1024, bar_at(sm, BND_FULL + j));
+                bulk_g2s(bnd + 2048, xb + a.pair_elems - 256, 1024, bar_at(sm, BND_FULL + j));
+                bulk_g2s(bnd + 3072, yb + a.pair_elems - 256, 1024, bar_at(sm, BND_FULL + j));
+                // row (of 256 floats) of core n = 1..N-2 of this pair: (b pair_elems + 256 + (n - 1) 16384) / 256
+                const int64_t row0 = ((int64_t)c.b * a.pair_elems + 256) / 256;
+                for (int n = 0; n < steps; ++n) {
+                    const int row = (int)(row0 + 64 * n);
+                    for (int t = 0; t < kTilesPerStep; ++t, ++k) {
+                        const int s = k % kRaw;
+                        mbar_wait(bar_at(sm, EMPTY + s), ((k / kRaw) & 1) ^ 1);
+                        unsigned char* dst = sm + kOffRaw + s * kTile;
+                        uint64_t* fb = bar_at(sm, FULL + s);
+                        mbar_arrive_expect_tx(fb, kTile);
+                        if (t < 4) {   // Y half t/2, K-chunk t%2: box (32 p, 2 i, 64 q)
+                            tma_3d(dst, &tmy, 32 * (t & 1), 2 * (t >> 1), row, fb);
+                        } else {       // X slice t-4: two boxes (32 r, 64 s)
+                            const int i = t - 4;
+                            tma_2d(dst, &tmx, 64 * i, row, fb);
+                            tma_2d(dst + 8192, &tmx, 64 * i + 32, row, fb);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================================================================ MMA issuer
+        if (lane == 0) {
+            const uint32_t id1 = idesc_tf32(128, 64), id2 = idesc_tf32(64, 64);
+            const uint32_t sbase = smem_u32(sm);
+            const uint32_t b1r = sbase + kOffB1, b1l = b1r + kTile;
+            uint32_t k = 0, v = 0;   // tile counter, interior-step counter
+            Cursor c;
+            for (int it = 0;; ++it) {
+                pair_at(a, it, c);
+                if (!c.valid) break;
+                for (int n = 0; n < steps; ++n, ++v) {
+                    mbar_wait(bar_at(sm, B1_READY), v & 1);
+                    // ---- GEMM-1, halves h = 0, 1 (M = 128: rows i' + 2q)
+                    for (int h = 0; h < 2; ++h) {
+                        mbar_wait(bar_at(sm, D1_EMPTY + h), (v & 1) ^ 1);
+                        uint32_t ar[2], al[2];
+                        for (int kc = 0; kc < 2; ++kc, ++k) {
+                            mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1);
+                            mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1);
+                            ar[kc] = sbase + kOffRaw + (k % kRaw) * kTile;
+                            al[kc] = sbase + kOffLo + (k % kLo) * kTile;
+                        }
+                        tc_fence_after();
+                        const uint32_t dm = tmem + kD1M + 64 * h, dl = tmem + kD1L + 64 * h;
+                        for (int kc = 0; kc < 2; ++kc)
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t A = desc_sw128(ar[kc] + 32 * kk), Al = desc_sw128(al[kc] + 32 * kk);
+                                const uint64_t Bm = desc_sw128(b1r + 8192 * kc + 32 * kk);
+                                const uint64_t Bl = desc_sw128(b1l + 8192 * kc + 32 * kk);
+                                mma_tf32(dm, A, Bm, id1, (kc | kk) ? 1u : 0u);
+                                mma_tf32(dl, Al, Bm, id1, (kc | kk) ? 1u : 0u);
+                                mma_tf32(dl, A, Bl, id1, 1u);
+                            }
+                        for (int kc = 0; kc < 2; ++kc) {
+                            const uint32_t kt = k - 2 + kc;
+                            mma_commit(bar_at(sm, EMPTY + kt % kRaw));
+                            mma_commit(bar_at(sm, LO_FREE + kt % kLo));
+                        }
+                        mma_commit(bar_at(sm, D1_FULL + h));
+                    }
+                    // ---- GEMM-2, slices i = 0..3 (M = 64), accumulated in D2
+                    for (int i = 0; i < 4; ++i, ++k) {
+                        const int j = i & 1;
+                        mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1);
+                        mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1);
+                        mbar_wait(bar_at(sm, B2_READY + j), (2 * v + (i >> 1)) & 1);
+                        mbar_wait(bar_at(sm, D2P_EMPTY + j), ((2 * v + (i >> 1)) & 1) ^ 1);
+                        tc_fence_after();
+                        const uint32_t ar = sbase + kOffRaw + (k % kRaw) * kTile;
+                        const uint32_t al = sbase + kOffLo + (k % kLo) * kTile;
+                        const uint32_t br = sbase + kOffB2 + j * 2 * kTile, bl = br + kTile;
+                        const uint32_t dl = tmem + kD2L;
+                        for (int kc = 0; kc < 2; ++kc) {
+                            const uint32_t dm = tmem + kD2P + 64 * j + ((uint32_t)(16 * kc) << 16);
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t A = desc_sw128(ar + 8192 * kc + 32 * kk);
+                                const uint64_t Al = desc_sw128(al + 8192 * kc + 32 * kk);
+                                const uint64_t Bm = desc_sw128(br + 8192 * kc + 32 * kk);
+                                const uint64_t Bl = desc_sw128(bl + 8192 * kc + 32 * kk);
+                                mma_tf32(dm, A, Bm, id2, kk ? 1u : 0u);
+                                mma_tf32(dl, Al, Bm, id2, (i | kc | kk) ? 1u : 0u);
+                                mma_tf32(dl, A, Bl, id2, 1u);
+                            }
+                        }
+                        mma_commit(bar_at(sm, EMPTY + k % kRaw));
+                        mma_commit(bar_at(sm, LO_FREE + k % kLo));
+                        mma_commit(bar_at(sm, B2_FREE + j));
+                        mma_commit(bar_at(sm, D2P_FULL + j));
+                        if (i == 3) mma_commit(bar_at(sm, D2_FULL));
+                    }
+                }
+            }
+        }
+    } else if (warp >= 6) {
+        // ================================================================ lo workers (warps 6, 7)
+        // the lo part of every staged input tile, in the order the MMA issuer consumes them (elementwise: the lo
+        // tile has the raw tile's byte layout); all loads of a thread's share are issued before any store
+        const int ct = threadIdx.x - 192;         // 0..63
+        uint32_t ktot = 0;
+        for (int idx = blockIdx.x; idx < a.B; idx += gridDim.x) ktot += (uint32_t)steps * kTilesPerStep;
+        for (uint32_t k = 0; k < ktot; ++k) {
+            const int s = k % kRaw, l = k % kLo;
+            mbar_wait(bar_at(sm, FULL + s), (k / kRaw) & 1);
+            mbar_wait(bar_at(sm, LO_FREE + l), ((k / kLo) & 1) ^ 1);
+            const float4* src = reinterpret_cast<const float4*>(sm + kOffRaw + s * kTile);
+            float4* dst = reinterpret_cast<float4*>(sm + kOffLo + l * kTile);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                float4 r[kTile / 16 / 128];
+#pragma unroll
+                for (int e = 0; e < kTile / 16 / 128; ++e) r[e] = src[ct + 64 * (2 * e + hf)];
+#pragma unroll
+                for (int e = 0; e < kTile / 16 / 128; ++e) dst[ct + 64 * (2 * e + hf)] = lo_rn4(r[e]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_at(sm, LO_READY + l));
+        }
+    } else {
+        // ================================================================ epilogue warps (warps 2..5)
+        const int ct = threadIdx.x - 64;          // 0..127
+        const int sp = warp & 3;                  // TMEM sub-partition of this warp (lanes 32 sp .. 32 sp + 31)
+        const uint32_t tl = tmem + ((uint32_t)(32 * sp) << 16);
+        unsigned char* b1r = sm + kOffB1;
+        unsigned char* b1l = b1r + kTile;
+        float* red = reinterpret_cast<float*>(sm + kOffRed);
+        uint32_t v = 0;
+        Cursor c;
+        for (int it = 0;; ++it) {
+            pair_at(a, it, c);
+            if (!c.valid) break;
+            const int jb = it & 1;
+            const float* bnd = reinterpret_cast<const float*>(sm + kOffBnd + jb * 4096);
+            mbar_wait(bar_at(sm, BND_FULL + jb), (it >> 1) & 1);
+            // ---- first step: Z_1[s][q] = sum_i X_1[0, i, s] Y_1[0, i, q]  (Eq. 12's K), into B1 (raw, lo)
+            {
+                const int s = ct >> 1, q0 = 32 * (ct & 1);
+                const float4 xs = reinterpret_cast<const float4*>(bnd)[s];
+                uint32_t zv[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const float4 yq = reinterpret_cast<const float4*>(bnd + 256)[q0 + q];
+                    float z = xs.x * yq.x;
+                    z = fmaf(xs.y, yq.y, z);
+                    z = fmaf(xs.z, yq.z, z);
+                    z = fmaf(xs.w, yq.w, z);
+                    zv[q] = __float_as_uint(z);
+                }
+#pragma unroll
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    const float4 f = make_float4(__uint_as_float(zv[4 * c4]), __uint_as_float(zv[4 * c4 + 1]),
+                                                 __uint_as_float(zv[4 * c4 + 2]), __uint_as_float(zv[4 * c4 + 3]));
+                    const uint32_t off = sw_off(s, q0 + 4 * c4, 64);
+                    float4 h, l;
+                    split_rn4(f, h, l);
+                    *reinterpret_cast<float4*>(b1r + off) = h;
+                    *reinterpret_cast<float4*>(b1l + off) = l;
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_at(sm, B1_READY));
+            }
+            for (int n = 0; n < steps; ++n, ++v) {
+                // ---- epilogue 1a: D1[0] (main + cross terms) -> W_0 (even lanes), W_1 (odd lanes) into B2[0], B2[1]
+                const int q = 16 * sp + (lane >> 1), ip = lane & 1;
+                // W row of this lane from D1[h] (a_hi b_hi partial + cross terms), 32 columns at a time, split and
+                // written to B2[j] by the lanes with ip == j (tcgen05.ld is warp-collective: every lane loads)
+                auto write_w = [&](int h, int jmask) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        uint32_t t0[32], t1[32];
+                        tmem_ld32(tl + kD1M + 64 * h + 32 * hh, t0);
+                        tmem_ld32(tl + kD1L + 64 * h + 32 * hh, t1);
+                        tmem_wait_ld();
+                        if ((jmask >> ip) & 1) {
+                            unsigned char* br = sm + kOffB2 + ip * 2 * kTile;
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {
+                                float4 f;
+                                f.x = __uint_as_float(t0[4 * c]) + __uint_as_float(t1[4 * c]);
+                                f.y = __uint_as_float(t0[4 * c + 1]) + __uint_as_float(t1[4 * c + 1]);
+                                f.z = __uint_as_float(t0[4 * c + 2]) + __uint_as_float(t1[4 * c + 2]);
+                                f.w = __uint_as_float(t0[4 * c + 3]) + __uint_as_float(t1[4 * c + 3]);
+                                float4 hi, lo;
+                                split_rn4(f, hi, lo);
+                                const uint32_t off = sw_off(q, 32 * hh + 4 * c, 64);
+                                *reinterpret_cast<float4*>(br + off) = hi;
+                                *reinterpret_cast<float4*>(br + kTile + off) = lo;
+                            }
+                        }
+                    }
+                };
+                // GEMM-2 slice partials: lanes 0..15 accumulate K-chunk 0, lanes 16..31 K-chunk 1 of row 16 sp + lane % 16
+                float zacc[64];
+                auto add_slice = [&](int i) {
+                    const int j = i & 1;
+                    mbar_wait(bar_at(sm, D2P_FULL + j), (2 * v + (i >> 1)) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        uint32_t p0[32];
+                        tmem_ld32(tl + kD2P + 64 * j + 32 * hh, p0);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            zacc[32 * hh + e] = i ? zacc[32 * hh + e] + __uint_as_float(p0[e]) : __uint_as_float(p0[e]);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_at(sm, D2P_EMPTY + j));
+                };
+                mbar_wait(bar_at(sm, D1_FULL + 0), v & 1);
+                mbar_wait(bar_at(sm, B2_FREE + 0), ((2 * v) & 1) ^ 1);
+                mbar_wait(bar_at(sm, B2_FREE + 1), ((2 * v) & 1) ^ 1);
+                tc_fence_after();
+                write_w(0, 3);
+                tc_fence_before();
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(bar_at(sm, D1_EMPTY + 0));
+                    mbar_arrive(bar_at(sm, B2_READY + 0));
+                    mbar_arrive(bar_at(sm, B2_READY + 1));
+                }
+                // ---- epilogue 1b: D1[1] -> W_2 into B2[0] (after GEMM-2 slice 0), W_3 into B2[1] (after slice 1)
+                mbar_wait(bar_at(sm, D1_FULL + 1), v & 1);
+                for (int j = 0; j < 2; ++j) {
+                    mbar_wait(bar_at(sm, B2_FREE + j), ((2 * v + 1) & 1) ^ 1);
+                    add_slice(j);                                 // slice j is done (B2[j] is free)
+                    tc_fence_after();
+                    write_w(1, 1 << j);
+                    tc_fence_before();
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(bar_at(sm, B2_READY + j));
+                        if (j == 1) mbar_arrive(bar_at(sm, D1_EMPTY + 1));
+                    }
+                }
+                add_slice(2);
+                add_slice(3);
+                // ---- epilogue 2: Z_n = (chunk-0 sums + chunk-1 sums) + cross terms (rows s = 16 sp + lane, lane < 16)
+                mbar_wait(bar_at(sm, D2_FULL), v & 1);
+                tc_fence_after();
+                uint32_t z0[32], z1[32];
+                tmem_ld32(tl + kD2L, z0);
+                tmem_ld32(tl + kD2L + 32, z1);
+                tmem_wait_ld();
+                tc_fence_before();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const float a0 = zacc[e] + __shfl_down_sync(0xffffffffu, zacc[e], 16);
+                    const float a1 = zacc[32 + e] + __shfl_down_sync(0xffffffffu, zacc[32 + e], 16);
+                    z0[e] = __float_as_uint(a0 + __uint_as_float(z0[e]));
+                    z1[e] = __float_as_uint(a1 + __uint_as_float(z1[e]));
+                }
+                const int s = 16 * sp + lane;
+                if (n + 1 < steps) {
+                    if (lane < 16) write_row64(b1r, b1l, s, z0, z1);
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_at(sm, B1_READY));
+                } else {
+                    // ---- last step: out = sum_{s,q} Z[s][q] sum_i X_N[s, i, 0] Y_N[q, i, 0]
+                    float acc = 0.f;
+                    if (lane < 16) {
+                        const float* xN = bnd + 512;
+                        const float* yN = bnd + 768;
+                        const float x0 = xN[s], x1 = xN[s + 64], x2 = xN[s + 128], x3 = xN[s + 192];
+#pragma unroll
+                        for (int qq = 0; qq < 64; ++qq) {
+                            float t = x0 * yN[qq];
+                            t = fmaf(x1, yN[qq + 64], t);
+                            t = fmaf(x2, yN[qq + 128], t);
+                            t = fmaf(x3, yN[qq + 192], t);
+                            acc = fmaf(__uint_as_float(qq < 32 ? z0[qq & 31] : z1[qq & 31]), t, acc);
+                        }
+                    }
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    if (lane == 0) red[sp] = acc;
+                    bar_named(1, 128);
+                    if (ct == 0) a.out[c.b] = (red[0] + red[1]) + (red[2] + red[3]);
+                    bar_named(1, 128);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_at(sm, BND_EMPTY + jb));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(kTmemCols));
+}
+
+// ---- host: tensor maps through the driver entry point (no link-time dependency on libcuda)
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+bool inner_r64tc_supported(const InnerArgs& a, bool uniform_r64) {
+    if (!uniform_r64 || a.N < 3 || a.x.offsets || a.y.offsets) return false;
+    for (int n = 0; n < a.N; ++n)
+        if (a.dims[n] != 4) return false;
+    if ((reinterpret_cast<uintptr_t>(a.x.cores) | reinterpret_cast<uintptr_t>(a.y.cores)) & 15u) return false;
+    const int64_t rows = (int64_t)a.B * a.x.train_elems / 256;
+    return rows < (int64_t(1) << 31);
+}
+
+cudaError_t launch_inner_r64tc(const InnerArgs& a, cudaStream_t s) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const int64_t pe = a.x.train_elems;            // 256 + (N - 2) 16384 + 256 floats per train
+    const cuuint64_t rows = (cuuint64_t)((int64_t)a.B * pe / 256);
+    CUtensorMap tmx, tmy;
+    {   // X: rows of 256 floats (r + 64 i for one s), box 32 x 64 rows
+        const cuuint64_t dims[2] = {256, rows};
+        const cuuint64_t strides[1] = {1024};
+        const cuuint32_t box[2] = {32, 64};
+        const cuuint32_t es[2] = {1, 1};
+        if (enc(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.x.cores), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    {   // Y: (p: 64, i: 4 @ 256 B, q-row: rows @ 1024 B), box (32 p, 2 i, 64 q) -> SMEM rows i' + 2 q
+        const cuuint64_t dims[3] = {64, 4, rows};
+        const cuuint64_t strides[2] = {256, 1024};
+        const cuuint32_t box[3] = {32, 2, 64};
+        const cuuint32_t es[3] = {1, 1, 1};
+        if (enc(&tmy, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a.y.cores), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    TcArgs t;
+    t.B = a.B;
+    t.N = a.N;
+    t.pair_elems = pe;
+    t.x = a.x.cores;
+    t.y = a.y.cores;
+    t.out = a.out;
+    t.order = a.order;
+    cudaError_t e = cudaFuncSetAttribute(inner_r64tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    const int grid = a.B < sms ? a.B : sms;
+    inner_r64tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(t, tmx, tmy);
+    return cudaGetLastError();
+}
+
+}  // namespace ttc

@@ -250,8 +250,8 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
     const bool uniform = hx.uniform && hy.uniform && hx.urank == hy.urank;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    // TTC_KERNEL=generic|fast|small|ffma forces the general-shape / CTA-per-pair tensor-core / tiny-batch /
-    // warp-per-pair FP32 kernel (cross-checks and A/B measurements)
+    // TTC_KERNEL=generic|fast|small|ffma|mmasync forces the general-shape / CTA-per-pair tensor-core / tiny-batch /
+    // warp-per-pair FP32 / legacy mma.sync rank-64 kernel (cross-checks and A/B measurements)
     const char* kv = std::getenv("TTC_KERNEL");
     const bool force_generic = kv && std::strcmp(kv, "generic") == 0;
     // uniform rank-16 trains with 16-byte aligned cores and trains: the specialised rank-16 kernel
@@ -263,6 +263,7 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
     const bool uniform_r16 = uniform && hx.urank == 16 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     const bool force_fast = kv && std::strcmp(kv, "fast") == 0;
     const bool force_ffma = kv && std::strcmp(kv, "ffma") == 0;
+    const bool force_mma_sync = kv && std::strcmp(kv, "mmasync") == 0;   // rank 64: the mma.sync kernel
     const bool uniform_r64 = uniform && hx.urank == 64 && aligned16 && (hx.train_elems_uniform & 3) == 0;
     // tiny batches are latency-bound: both trains of a pair staged at once, one DRAM round trip per pair
     // (TTC_KERNEL=small forces it for any batch that fits, for cross-checks)
@@ -295,8 +296,10 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
         e = ttc::launch_inner_ffma(a, mr, s);
     else if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
         e = ttc::launch_inner_r16(a, s);
+    else if (!force_generic && !force_mma_sync && ttc::inner_r64tc_supported(a, uniform_r64))
+        e = ttc::launch_inner_r64tc(a, s);     // tcgen05.mma kind::tf32, TMEM accumulators, TMA operands
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
-        e = ttc::launch_inner_r64(a, s);
+        e = ttc::launch_inner_r64(a, s);       // legacy mma.sync 3xTF32 (any I_n, offsets allowed)
     else if (!force_generic && !force_fast && ffma_ok)
         e = ttc::launch_inner_ffma(a, mr, s);   // warp per pair on the FP32 pipe (ranks multiple of 8, <= 32)
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))

@@ -35,6 +35,9 @@ bool        inner_r16_supported(const InnerArgs& a, bool uniform_r16);
 cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s);
 bool        inner_r64_supported(const InnerArgs& a, bool uniform_r64);
 cudaError_t launch_inner_r64(const InnerArgs& a, cudaStream_t s);
+// uniform rank 64, I_n = 4, packed trains: tcgen05 / TMEM / TMA kernel (inner_r64tc.cu)
+bool        inner_r64tc_supported(const InnerArgs& a, bool uniform_r64);
+cudaError_t launch_inner_r64tc(const InnerArgs& a, cudaStream_t s);
 // tiny batches (inner_small.cu): both trains of a pair in SMEM at once; floats of each region
 struct SmallLayout {
     int32_t xmax, ymax, wmax, zmax;

@@ -307,3 +307,21 @@ def test_cost_ordered_inner_is_bitwise_equal():
         assert sorted(order.host.tolist()) == list(range(B))
         got = ttc.ttc_inner(XD, YD, order=order).cpu().numpy()
         assert np.array_equal(ref.view(np.uint32), got.view(np.uint32)), cfg
+
+
+@pytest.mark.parametrize("N,B", [(3, 1), (3, 149), (4, 2), (16, 150), (16, 297), (21, 37)])
+def test_r64_tcgen05_kernel(monkeypatch, N, B):
+    """The tcgen05 rank-64 kernel (inner_r64tc.cu: uniform R = 64, I_n = 4, packed) on one interior step (N = 3),
+    batches below / just above / about twice the CTA count (static pair assignment), and long chains (N = 21):
+    self and correlated pairs against the oracle (1e-5 |oracle| gate) and against the legacy mma.sync kernel
+    (TTC_KERNEL=mmasync) within fp32 rounding."""
+    r = ttgen.uniform_ranks(B, N, 64)
+    for kind in ("self", "corr"):
+        X, Y = ttgen.make_pair(kind, 11 + N, 4, 0, r, (4,) * N, device=DEV)
+        got = _run(X, Y)
+        _check(X, Y, got, _sample(B, 12, N), kind)
+        monkeypatch.setenv("TTC_KERNEL", "mmasync")
+        ref = _run(X, Y)
+        monkeypatch.delenv("TTC_KERNEL")
+        for b in range(B):
+            assert abs(got[b] - ref[b]) <= 2e-5 * abs(ref[b]), (kind, b, got[b], ref[b])

@@ -15,7 +15,7 @@ OURS = re.compile(r"ttc::|inner_|contract_kernel|splice_kernel|reconstruct_kerne
 
 
 def short(name):
-    m = re.search(r"(inner_r16_kernel|inner_r64_kernel|inner_ffma_kernel|inner_wpp_kernel<[^>]*>|inner_tc_kernel<[^>]*>|inner_generic_kernel|contract_kernel|splice_kernel|reconstruct_kernel|ttsvd_kernel)", name)
+    m = re.search(r"(inner_r16_kernel|inner_r64_kernel|inner_r64tc_kernel|inner_ffma_kernel|inner_tc_kernel<[^>]*>|inner_generic_kernel|contract_kernel|splice_kernel|reconstruct_kernel|ttsvd_kernel)", name)
     return m.group(1) if m else name.split("(")[0][-60:]
 
 

@@ -183,7 +183,52 @@ void run(int chain, int timed, bool exact_inputs, unsigned seed) {
     CK(cudaFree(dA)); CK(cudaFree(dB)); CK(cudaFree(dD)); CK(cudaFree(dc));
 }
 
+// accumulation rounding mode: all-positive tf32-exact inputs (no cancellation), mean signed relative error of D
+// against the exact sum, next to fp32 models of the chain (K = 8 partial sums added with RN or with RZ)
+static float rz_add(float a, double b) {   // a + b truncated toward zero to fp32
+    double s = (double)a + b;
+    float f = (float)s;
+    if (fabs((double)f) > fabs(s)) f = nextafterf(f, 0.f);
+    return f;
+}
+template <int M, int N>
+void bias(int chain) {
+    std::vector<float> A(M * 32), B(N * 32), D(M * N);
+    srand(77 + chain);
+    for (auto& x : A) x = trunc_tf32(0.5f + 0.5f * rand() / (float)RAND_MAX);
+    for (auto& x : B) x = trunc_tf32(0.5f + 0.5f * rand() / (float)RAND_MAX);
+    float *dA, *dB, *dD; long long* dc;
+    CK(cudaMalloc(&dA, A.size() * 4)); CK(cudaMalloc(&dB, B.size() * 4)); CK(cudaMalloc(&dD, D.size() * 4)); CK(cudaMalloc(&dc, 64));
+    CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
+    const size_t smem = 1024 + (M + N) * 128;
+    CK(cudaFuncSetAttribute(probe_kernel<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    probe_kernel<M, N><<<1, 128, smem>>>(dA, dB, dD, chain, 0, dc);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+    double mg = 0, mrn = 0, mrz = 0;
+    for (int m = 0; m < M; ++m)
+        for (int n = 0; n < N; ++n) {
+            double ex = 0; float rn = 0.f, rz = 0.f;
+            for (int c = 0; c < chain; ++c)
+                for (int kb = 0; kb < 4; ++kb) {
+                    double part = 0;
+                    for (int k = 8 * kb; k < 8 * kb + 8; ++k) part += (double)A[m * 32 + k] * B[n * 32 + k];
+                    ex += part;
+                    rn = (float)((double)rn + part);
+                    rz = rz_add(rz, part);
+                }
+            mg += (D[m * N + n] - ex) / ex; mrn += (rn - ex) / ex; mrz += (rz - ex) / ex;
+        }
+    const double cnt = (double)M * N;
+    printf("bias M=%d N=%d %4d accumulations: mean rel err GPU %+.3e | model RN %+.3e | model RZ %+.3e\n", M, N, 4 * chain,
+           mg / cnt, mrn / cnt, mrz / cnt);
+    CK(cudaFree(dA)); CK(cudaFree(dB)); CK(cudaFree(dD)); CK(cudaFree(dc));
+}
+
 int main() {
+    for (int ch : {1, 4, 16, 64}) bias<64, 64>(ch);
+    bias<128, 64>(16);
     // (1) layout + input reduction (one chain of 4 MMAs, K = 32)
     run<64, 64>(1, 0, false, 1);
     run<128, 64>(1, 0, false, 2);
