@@ -25,6 +25,7 @@
 //            (Z_1 = A_x^T A_y, Eq. 12, and the final scalar) on the FP32 pipe
 //   warps 6-7 lo workers: the lo parts of the staged input tiles (3-buffer ring)
 #include <cuda.h>
+#include <cstdio>
 
 #include "tc_common.cuh"
 #include "ttc_internal.h"
@@ -42,8 +43,10 @@ constexpr int kTilesPerStep = 8;                  // Y halves (2 K-chunks each),
 // shared-memory layout (bytes from the 1024-aligned base)
 constexpr int kOffRaw = 0;
 constexpr int kOffLo = kOffRaw + kRaw * kTile;
-constexpr int kOffB2 = kOffLo + kLo * kTile;      // 2 buffers x {raw 16 KB, lo 16 KB}: W_i as the GEMM-2 B operand
-constexpr int kOffB1 = kOffB2 + 4 * kTile;        // {raw 16 KB, lo 16 KB}: Z as the GEMM-1 B operand
+// B operands written by the threads (32 KB each): per 32-wide K-chunk kc, 64 hi rows then 64 lo rows (16 KB), so
+// that one N = 128 MMA reads [B_hi | B_lo] and one N = 64 MMA reads B_hi
+constexpr int kOffB2 = kOffLo + kLo * kTile;      // 2 buffers: W_i as the GEMM-2 B operand (buffer i & 1)
+constexpr int kOffB1 = kOffB2 + 4 * kTile;        // Z as the GEMM-1 B operand
 constexpr int kOffBnd = kOffB1 + 2 * kTile;       // 2 buffers x {X_1, Y_1, X_N, Y_N} x 1 KB
 constexpr int kOffRed = kOffBnd + 2 * 4096;       // 4 floats: the final reduction
 constexpr int kOffBar = kOffRed + 64;
@@ -59,11 +62,18 @@ constexpr int FULL = 0, EMPTY = 4, LO_READY = 8, LO_FREE = 11, D1_FULL = 14, D1_
 // accumulate in short chains -- GEMM-1 8 MMAs per half, GEMM-2 4 per (slice, K-chunk) -- and the small cross terms
 // (2^-11 smaller, their truncation negligible) in separate accumulators; the converters add the partials in fp32
 // round-to-nearest.
+// Each accumulator is a 128-column block: a_hi b_hi in columns 0..63, the cross terms in 64..127 (one N = 128 MMA
+// a_hi [b_hi | b_lo] writes both, one N = 64 MMA adds a_lo b_hi to the second half).
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kD1M = 0;      // + 64 h: GEMM-1 a_hi b_hi, half h (M = 128)
-constexpr uint32_t kD1L = 128;    // + 64 h: GEMM-1 cross terms
-constexpr uint32_t kD2P = 256;    // + 64 (i & 1): GEMM-2 a_hi b_hi of slice i, K-chunk kc at lanes 16 kc + (0..15)
-constexpr uint32_t kD2L = 384;    // GEMM-2 cross terms of all four slices (M = 64: lanes 0..15)
+constexpr uint32_t kD1 = 0;       // + 128 h: GEMM-1 of half h (M = 128)
+constexpr uint32_t kD2 = 256;     // + 128 (i & 1): GEMM-2 of slice i (M = 64), K-chunk kc at lanes 16 kc + (0..15)
+
+// TTC_R64_PROF builds: clock64 time each role spends in each barrier wait, printed by CTA 0 at the end
+#ifdef TTC_R64_PROF
+#define PW(slot, call) do { const long long t0_ = clock64(); call; prof[slot] += clock64() - t0_; } while (0)
+#else
+#define PW(slot, call) call
+#endif
 
 struct TcArgs {
     int32_t B, N;
@@ -140,26 +150,33 @@ __device__ __forceinline__ void split_rn4(float4 v, float4& hi, float4& lo) {
     lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
 }
 
-// byte offset of element (row, k) in a K-major 128B-swizzled operand of 64-element rows stored as two 32-element
-// chunks of `rows` x 128 B each
-__device__ __forceinline__ uint32_t sw_off(int row, int k, int rows) {
-    return (uint32_t)((k >> 5) * rows * 128 + row * 128 + ((((k >> 2) & 7) ^ (row & 7)) << 4) + ((k & 3) << 2));
+// byte offset of the hi part of element (row, k) of a thread-written B operand (lo: + 8192)
+__device__ __forceinline__ uint32_t bb_off(int row, int k) {
+    return (uint32_t)((k >> 5) * 16384 + row * 128 + ((((k >> 2) & 7) ^ (row & 7)) << 4) + ((k & 3) << 2));
 }
-
-// one converter thread writes 64 values (row `row` of a 64-row operand, K = 0..63) as raw + lo
-__device__ __forceinline__ void write_row64(unsigned char* raw, unsigned char* lo, int row, const uint32_t (&v0)[32],
-                                            const uint32_t (&v1)[32]) {
+__device__ __forceinline__ float4 f4(const uint32_t* v) {
+    return make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
+}
+__device__ __forceinline__ float4 sel4(bool s, float4 a, float4 b) {
+    return make_float4(s ? a.x : b.x, s ? a.y : b.y, s ? a.z : b.z, s ? a.w : b.w);
+}
+// one thread writes 32 values (row `row`, K = k0 .. k0 + 31) of a B operand as hi + lo.  Within each pair of 16-byte
+// chunks, rows with bit 3 set store the odd chunk first: rows r and r + 8 (same swizzle phase) then never hit the
+// same bank group in one instruction (16 consecutive rows per warp store: conflict-free).
+__device__ __forceinline__ void write_b32(unsigned char* buf, int row, int k0, const float4 (&f)[8]) {
+    const bool sw = (row >> 3) & 1;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-        const uint32_t* src = c < 8 ? v0 : v1;
-        const int j = (c & 7) * 4;
-        float4 f = make_float4(__uint_as_float(src[j]), __uint_as_float(src[j + 1]), __uint_as_float(src[j + 2]),
-                               __uint_as_float(src[j + 3]));
-        const uint32_t off = sw_off(row, 4 * c, 64);
-        float4 h, l;
-        split_rn4(f, h, l);
-        *reinterpret_cast<float4*>(raw + off) = h;
-        *reinterpret_cast<float4*>(lo + off) = l;
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 2 * u + (e ^ (int)sw);
+            const float4 v = sel4(sw == (bool)e, f[2 * u], f[2 * u + 1]);   // chunk c's data
+            float4 h, l;
+            split_rn4(v, h, l);
+            const uint32_t off = bb_off(row, k0 + 4 * c);
+            *reinterpret_cast<float4*>(buf + off) = h;
+            *reinterpret_cast<float4*>(buf + off + 8192) = l;
+        }
     }
 }
 
@@ -205,6 +222,10 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+#ifdef TTC_R64_PROF
+    long long prof[20] = {0};
+    const long long tstart = clock64();
+#endif
 
     if (warp == 0) {
         // ================================================================ TMA producer
@@ -217,7 +238,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                 pair_at(a, it, c);
                 if (!c.valid) break;
                 const int j = it & 1;
-                mbar_wait(bar_at(sm, BND_EMPTY + j), ((it >> 1) & 1) ^ 1);
+                PW(0, mbar_wait(bar_at(sm, BND_EMPTY + j), ((it >> 1) & 1) ^ 1));
                 unsigned char* bnd = sm + kOffBnd + j * 4096;
                 const float* xb = a.x + (int64_t)c.b * a.pair_elems;
                 const float* yb = a.y + (int64_t)c.b * a.pair_elems;
@@ -232,7 +253,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                     const int row = (int)(row0 + 64 * n);
                     for (int t = 0; t < kTilesPerStep; ++t, ++k) {
                         const int s = k % kRaw;
-                        mbar_wait(bar_at(sm, EMPTY + s), ((k / kRaw) & 1) ^ 1);
+                        PW(1, mbar_wait(bar_at(sm, EMPTY + s), ((k / kRaw) & 1) ^ 1));
                         unsigned char* dst = sm + kOffRaw + s * kTile;
                         uint64_t* fb = bar_at(sm, FULL + s);
                         mbar_arrive_expect_tx(fb, kTile);
@@ -250,36 +271,35 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
     } else if (warp == 1) {
         // ================================================================ MMA issuer
         if (lane == 0) {
-            const uint32_t id1 = idesc_tf32(128, 64), id2 = idesc_tf32(64, 64);
+            const uint32_t id1w = idesc_tf32(128, 128), id1 = idesc_tf32(128, 64);
+            const uint32_t id2w = idesc_tf32(64, 128), id2 = idesc_tf32(64, 64);
             const uint32_t sbase = smem_u32(sm);
-            const uint32_t b1r = sbase + kOffB1, b1l = b1r + kTile;
+            const uint32_t b1 = sbase + kOffB1;
             uint32_t k = 0, v = 0;   // tile counter, interior-step counter
             Cursor c;
             for (int it = 0;; ++it) {
                 pair_at(a, it, c);
                 if (!c.valid) break;
                 for (int n = 0; n < steps; ++n, ++v) {
-                    mbar_wait(bar_at(sm, B1_READY), v & 1);
+                    PW(2, mbar_wait(bar_at(sm, B1_READY), v & 1));
                     // ---- GEMM-1, halves h = 0, 1 (M = 128: rows i' + 2q)
                     for (int h = 0; h < 2; ++h) {
-                        mbar_wait(bar_at(sm, D1_EMPTY + h), (v & 1) ^ 1);
+                        PW(3, mbar_wait(bar_at(sm, D1_EMPTY + h), (v & 1) ^ 1));
                         uint32_t ar[2], al[2];
                         for (int kc = 0; kc < 2; ++kc, ++k) {
-                            mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1);
-                            mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1);
+                            PW(4, mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1));
+                            PW(5, mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1));
                             ar[kc] = sbase + kOffRaw + (k % kRaw) * kTile;
                             al[kc] = sbase + kOffLo + (k % kLo) * kTile;
                         }
                         tc_fence_after();
-                        const uint32_t dm = tmem + kD1M + 64 * h, dl = tmem + kD1L + 64 * h;
+                        const uint32_t d = tmem + kD1 + 128 * h;
                         for (int kc = 0; kc < 2; ++kc)
                             for (int kk = 0; kk < 4; ++kk) {
                                 const uint64_t A = desc_sw128(ar[kc] + 32 * kk), Al = desc_sw128(al[kc] + 32 * kk);
-                                const uint64_t Bm = desc_sw128(b1r + 8192 * kc + 32 * kk);
-                                const uint64_t Bl = desc_sw128(b1l + 8192 * kc + 32 * kk);
-                                mma_tf32(dm, A, Bm, id1, (kc | kk) ? 1u : 0u);
-                                mma_tf32(dl, Al, Bm, id1, (kc | kk) ? 1u : 0u);
-                                mma_tf32(dl, A, Bl, id1, 1u);
+                                const uint64_t B = desc_sw128(b1 + 16384 * kc + 32 * kk);   // [Z_hi | Z_lo]
+                                mma_tf32(d, A, B, id1w, (kc | kk) ? 1u : 0u);             // a_hi [b_hi | b_lo]
+                                mma_tf32(d + 64, Al, B, id1, 1u);                         // + a_lo b_hi
                             }
                         for (int kc = 0; kc < 2; ++kc) {
                             const uint32_t kt = k - 2 + kc;
@@ -291,32 +311,28 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                     // ---- GEMM-2, slices i = 0..3 (M = 64), accumulated in D2
                     for (int i = 0; i < 4; ++i, ++k) {
                         const int j = i & 1;
-                        mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1);
-                        mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1);
-                        mbar_wait(bar_at(sm, B2_READY + j), (2 * v + (i >> 1)) & 1);
-                        mbar_wait(bar_at(sm, D2P_EMPTY + j), ((2 * v + (i >> 1)) & 1) ^ 1);
+                        PW(6, mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1));
+                        PW(7, mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1));
+                        PW(8, mbar_wait(bar_at(sm, B2_READY + j), (2 * v + (i >> 1)) & 1));
+                        PW(9, mbar_wait(bar_at(sm, D2P_EMPTY + j), ((2 * v + (i >> 1)) & 1) ^ 1));
                         tc_fence_after();
                         const uint32_t ar = sbase + kOffRaw + (k % kRaw) * kTile;
                         const uint32_t al = sbase + kOffLo + (k % kLo) * kTile;
-                        const uint32_t br = sbase + kOffB2 + j * 2 * kTile, bl = br + kTile;
-                        const uint32_t dl = tmem + kD2L;
+                        const uint32_t br = sbase + kOffB2 + j * 2 * kTile;
                         for (int kc = 0; kc < 2; ++kc) {
-                            const uint32_t dm = tmem + kD2P + 64 * j + ((uint32_t)(16 * kc) << 16);
+                            const uint32_t d = tmem + kD2 + 128 * j + ((uint32_t)(16 * kc) << 16);
                             for (int kk = 0; kk < 4; ++kk) {
                                 const uint64_t A = desc_sw128(ar + 8192 * kc + 32 * kk);
                                 const uint64_t Al = desc_sw128(al + 8192 * kc + 32 * kk);
-                                const uint64_t Bm = desc_sw128(br + 8192 * kc + 32 * kk);
-                                const uint64_t Bl = desc_sw128(bl + 8192 * kc + 32 * kk);
-                                mma_tf32(dm, A, Bm, id2, kk ? 1u : 0u);
-                                mma_tf32(dl, Al, Bm, id2, (i | kc | kk) ? 1u : 0u);
-                                mma_tf32(dl, A, Bl, id2, 1u);
+                                const uint64_t B = desc_sw128(br + 16384 * kc + 32 * kk);   // [W_hi | W_lo]
+                                mma_tf32(d, A, B, id2w, kk ? 1u : 0u);
+                                mma_tf32(d + 64, Al, B, id2, 1u);
                             }
                         }
                         mma_commit(bar_at(sm, EMPTY + k % kRaw));
                         mma_commit(bar_at(sm, LO_FREE + k % kLo));
                         mma_commit(bar_at(sm, B2_FREE + j));
                         mma_commit(bar_at(sm, D2P_FULL + j));
-                        if (i == 3) mma_commit(bar_at(sm, D2_FULL));
                     }
                 }
             }
@@ -330,8 +346,8 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
         for (int idx = blockIdx.x; idx < a.B; idx += gridDim.x) ktot += (uint32_t)steps * kTilesPerStep;
         for (uint32_t k = 0; k < ktot; ++k) {
             const int s = k % kRaw, l = k % kLo;
-            mbar_wait(bar_at(sm, FULL + s), (k / kRaw) & 1);
-            mbar_wait(bar_at(sm, LO_FREE + l), ((k / kLo) & 1) ^ 1);
+            PW(10, mbar_wait(bar_at(sm, FULL + s), (k / kRaw) & 1));
+            PW(11, mbar_wait(bar_at(sm, LO_FREE + l), ((k / kLo) & 1) ^ 1));
             const float4* src = reinterpret_cast<const float4*>(sm + kOffRaw + s * kTile);
             float4* dst = reinterpret_cast<float4*>(sm + kOffLo + l * kTile);
 #pragma unroll
@@ -351,8 +367,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
         const int ct = threadIdx.x - 64;          // 0..127
         const int sp = warp & 3;                  // TMEM sub-partition of this warp (lanes 32 sp .. 32 sp + 31)
         const uint32_t tl = tmem + ((uint32_t)(32 * sp) << 16);
-        unsigned char* b1r = sm + kOffB1;
-        unsigned char* b1l = b1r + kTile;
+        unsigned char* b1 = sm + kOffB1;
         float* red = reinterpret_cast<float*>(sm + kOffRed);
         uint32_t v = 0;
         Cursor c;
@@ -361,7 +376,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
             if (!c.valid) break;
             const int jb = it & 1;
             const float* bnd = reinterpret_cast<const float*>(sm + kOffBnd + jb * 4096);
-            mbar_wait(bar_at(sm, BND_FULL + jb), (it >> 1) & 1);
+            PW(12, mbar_wait(bar_at(sm, BND_FULL + jb), (it >> 1) & 1));
             // ---- first step: Z_1[s][q] = sum_i X_1[0, i, s] Y_1[0, i, q]  (Eq. 12's K), into B1 (raw, lo)
             {
                 const int s = ct >> 1, q0 = 32 * (ct & 1);
@@ -376,16 +391,10 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                     z = fmaf(xs.w, yq.w, z);
                     zv[q] = __float_as_uint(z);
                 }
+                float4 f[8];
 #pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4) {
-                    const float4 f = make_float4(__uint_as_float(zv[4 * c4]), __uint_as_float(zv[4 * c4 + 1]),
-                                                 __uint_as_float(zv[4 * c4 + 2]), __uint_as_float(zv[4 * c4 + 3]));
-                    const uint32_t off = sw_off(s, q0 + 4 * c4, 64);
-                    float4 h, l;
-                    split_rn4(f, h, l);
-                    *reinterpret_cast<float4*>(b1r + off) = h;
-                    *reinterpret_cast<float4*>(b1l + off) = l;
-                }
+                for (int c4 = 0; c4 < 8; ++c4) f[c4] = f4(zv + 4 * c4);
+                write_b32(b1, s, q0, f);
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_at(sm, B1_READY));
@@ -399,24 +408,19 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         uint32_t t0[32], t1[32];
-                        tmem_ld32(tl + kD1M + 64 * h + 32 * hh, t0);
-                        tmem_ld32(tl + kD1L + 64 * h + 32 * hh, t1);
+                        tmem_ld32(tl + kD1 + 128 * h + 32 * hh, t0);
+                        tmem_ld32(tl + kD1 + 128 * h + 64 + 32 * hh, t1);
                         tmem_wait_ld();
                         if ((jmask >> ip) & 1) {
-                            unsigned char* br = sm + kOffB2 + ip * 2 * kTile;
+                            float4 f[8];
 #pragma unroll
                             for (int c = 0; c < 8; ++c) {
-                                float4 f;
-                                f.x = __uint_as_float(t0[4 * c]) + __uint_as_float(t1[4 * c]);
-                                f.y = __uint_as_float(t0[4 * c + 1]) + __uint_as_float(t1[4 * c + 1]);
-                                f.z = __uint_as_float(t0[4 * c + 2]) + __uint_as_float(t1[4 * c + 2]);
-                                f.w = __uint_as_float(t0[4 * c + 3]) + __uint_as_float(t1[4 * c + 3]);
-                                float4 hi, lo;
-                                split_rn4(f, hi, lo);
-                                const uint32_t off = sw_off(q, 32 * hh + 4 * c, 64);
-                                *reinterpret_cast<float4*>(br + off) = hi;
-                                *reinterpret_cast<float4*>(br + kTile + off) = lo;
+                                f[c].x = __uint_as_float(t0[4 * c]) + __uint_as_float(t1[4 * c]);
+                                f[c].y = __uint_as_float(t0[4 * c + 1]) + __uint_as_float(t1[4 * c + 1]);
+                                f[c].z = __uint_as_float(t0[4 * c + 2]) + __uint_as_float(t1[4 * c + 2]);
+                                f[c].w = __uint_as_float(t0[4 * c + 3]) + __uint_as_float(t1[4 * c + 3]);
                             }
+                            write_b32(sm + kOffB2 + ip * 2 * kTile, q, 32 * hh, f);
                         }
                     }
                 };
@@ -424,24 +428,27 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                 float zacc[64];
                 auto add_slice = [&](int i) {
                     const int j = i & 1;
-                    mbar_wait(bar_at(sm, D2P_FULL + j), (2 * v + (i >> 1)) & 1);
+                    PW(13, mbar_wait(bar_at(sm, D2P_FULL + j), (2 * v + (i >> 1)) & 1));
                     tc_fence_after();
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
-                        uint32_t p0[32];
-                        tmem_ld32(tl + kD2P + 64 * j + 32 * hh, p0);
+                        uint32_t p0[32], p1[32];
+                        tmem_ld32(tl + kD2 + 128 * j + 32 * hh, p0);
+                        tmem_ld32(tl + kD2 + 128 * j + 64 + 32 * hh, p1);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            zacc[32 * hh + e] = i ? zacc[32 * hh + e] + __uint_as_float(p0[e]) : __uint_as_float(p0[e]);
+                        for (int e = 0; e < 32; ++e) {
+                            const float t = __uint_as_float(p0[e]) + __uint_as_float(p1[e]);
+                            zacc[32 * hh + e] = i ? zacc[32 * hh + e] + t : t;
+                        }
                     }
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bar_at(sm, D2P_EMPTY + j));
                 };
-                mbar_wait(bar_at(sm, D1_FULL + 0), v & 1);
-                mbar_wait(bar_at(sm, B2_FREE + 0), ((2 * v) & 1) ^ 1);
-                mbar_wait(bar_at(sm, B2_FREE + 1), ((2 * v) & 1) ^ 1);
+                PW(14, mbar_wait(bar_at(sm, D1_FULL + 0), v & 1));
+                PW(15, mbar_wait(bar_at(sm, B2_FREE + 0), ((2 * v) & 1) ^ 1));
+                PW(15, mbar_wait(bar_at(sm, B2_FREE + 1), ((2 * v) & 1) ^ 1));
                 tc_fence_after();
                 write_w(0, 3);
                 tc_fence_before();
@@ -453,9 +460,9 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                     mbar_arrive(bar_at(sm, B2_READY + 1));
                 }
                 // ---- epilogue 1b: D1[1] -> W_2 into B2[0] (after GEMM-2 slice 0), W_3 into B2[1] (after slice 1)
-                mbar_wait(bar_at(sm, D1_FULL + 1), v & 1);
+                PW(16, mbar_wait(bar_at(sm, D1_FULL + 1), v & 1));
                 for (int j = 0; j < 2; ++j) {
-                    mbar_wait(bar_at(sm, B2_FREE + j), ((2 * v + 1) & 1) ^ 1);
+                    PW(17, mbar_wait(bar_at(sm, B2_FREE + j), ((2 * v + 1) & 1) ^ 1));
                     add_slice(j);                                 // slice j is done (B2[j] is free)
                     tc_fence_after();
                     write_w(1, 1 << j);
@@ -470,23 +477,23 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                 add_slice(2);
                 add_slice(3);
                 // ---- epilogue 2: Z_n = (chunk-0 sums + chunk-1 sums) + cross terms (rows s = 16 sp + lane, lane < 16)
-                mbar_wait(bar_at(sm, D2_FULL), v & 1);
-                tc_fence_after();
-                uint32_t z0[32], z1[32];
-                tmem_ld32(tl + kD2L, z0);
-                tmem_ld32(tl + kD2L + 32, z1);
-                tmem_wait_ld();
-                tc_fence_before();
+                uint32_t z0[32], z1[32];     // (slice 3 read above: every MMA of the step is complete)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
-                    const float a0 = zacc[e] + __shfl_down_sync(0xffffffffu, zacc[e], 16);
-                    const float a1 = zacc[32 + e] + __shfl_down_sync(0xffffffffu, zacc[32 + e], 16);
-                    z0[e] = __float_as_uint(a0 + __uint_as_float(z0[e]));
-                    z1[e] = __float_as_uint(a1 + __uint_as_float(z1[e]));
+                    z0[e] = __float_as_uint(zacc[e] + __shfl_down_sync(0xffffffffu, zacc[e], 16));
+                    z1[e] = __float_as_uint(zacc[32 + e] + __shfl_down_sync(0xffffffffu, zacc[32 + e], 16));
                 }
                 const int s = 16 * sp + lane;
                 if (n + 1 < steps) {
-                    if (lane < 16) write_row64(b1r, b1l, s, z0, z1);
+                    if (lane < 16) {
+                        float4 f[8];
+#pragma unroll
+                        for (int c4 = 0; c4 < 8; ++c4) f[c4] = f4(z0 + 4 * c4);
+                        write_b32(b1, s, 0, f);
+#pragma unroll
+                        for (int c4 = 0; c4 < 8; ++c4) f[c4] = f4(z1 + 4 * c4);
+                        write_b32(b1, s, 32, f);
+                    }
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bar_at(sm, B1_READY));
@@ -518,6 +525,15 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
             }
         }
     }
+#ifdef TTC_R64_PROF
+    if (blockIdx.x == 0 && lane == 0 && (warp <= 2 || warp == 6)) {
+        prof[19] = clock64() - tstart;
+        printf("r64tc prof warp %d total %lld | %lld %lld | %lld %lld %lld %lld %lld %lld %lld %lld | %lld %lld | "
+               "%lld %lld %lld %lld %lld %lld %lld\n", warp, prof[19], prof[0], prof[1], prof[2], prof[3], prof[4],
+               prof[5], prof[6], prof[7], prof[8], prof[9], prof[10], prof[11], prof[12], prof[13], prof[14],
+               prof[15], prof[16], prof[17], prof[18]);
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(kTmemCols));
