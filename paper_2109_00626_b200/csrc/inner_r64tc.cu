@@ -6,8 +6,8 @@
 //
 // Interior step n, in two GEMM families (Eq. 2 layout: Y_n[p, i, q] at p + 64 i + 256 q, X_n[r, i, s] likewise):
 //   GEMM-1, per half h (slices i = 2h, 2h+1), M = 128:
-//       D1_h[m = i' + 2q][r] = sum_p Y_n[p, 2h+i', q] Z[r][p]          (= W_i[r][q], W_i = Z Y_n[:, i, :])
-//       A = the Y_n slice pair as 128 rows x 64 p (a 3-D TMA box: p fastest, then i', then q), B = Z (64 r x 64 p)
+//       D1_h[m = q + 64 i'][r] = sum_p Y_n[p, 2h+i', q] Z[r][p]        (= W_i[r][q], W_i = Z Y_n[:, i, :])
+//       A = the Y_n slice pair as 128 rows x 64 p (a 3-D TMA box: p fastest, then q, then i'), B = Z (64 r x 64 p)
 //   GEMM-2, per slice i, M = 64:
 //       D2[s][q] += sum_r X_n[r, i, s] W_i[r][q]                        (= Z_n after the four slices)
 //       A = X_n[:, i, :]^T as 64 rows s x 64 r (2-D TMA boxes), B = W_i (64 q x 64 r, written by threads)
@@ -206,7 +206,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar_at(sm, D2P_FULL + i), 1); mbar_init(bar_at(sm, D2P_EMPTY + i), 4);
             mbar_init(bar_at(sm, D1_FULL + i), 1); mbar_init(bar_at(sm, D1_EMPTY + i), 4);
-            mbar_init(bar_at(sm, B2_READY + i), 4); mbar_init(bar_at(sm, B2_FREE + i), 1);
+            mbar_init(bar_at(sm, B2_READY + i), 2); mbar_init(bar_at(sm, B2_FREE + i), 1);
             mbar_init(bar_at(sm, BND_FULL + i), 1); mbar_init(bar_at(sm, BND_EMPTY + i), 4);
         }
         mbar_init(bar_at(sm, D2_FULL), 1);
@@ -258,7 +258,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                         uint64_t* fb = bar_at(sm, FULL + s);
                         mbar_arrive_expect_tx(fb, kTile);
                         if (t < 4) {   // Y half t/2, K-chunk t%2: box (32 p, 2 i, 64 q)
-                            tma_3d(dst, &tmy, 32 * (t & 1), 2 * (t >> 1), row, fb);
+                            tma_3d(dst, &tmy, 32 * (t & 1), row, 2 * (t >> 1), fb);
                         } else {       // X slice t-4: two boxes (32 r, 64 s)
                             const int i = t - 4;
                             tma_2d(dst, &tmx, 64 * i, row, fb);
@@ -379,7 +379,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
             PW(12, mbar_wait(bar_at(sm, BND_FULL + jb), (it >> 1) & 1));
             // ---- first step: Z_1[s][q] = sum_i X_1[0, i, s] Y_1[0, i, q]  (Eq. 12's K), into B1 (raw, lo)
             {
-                const int s = ct >> 1, q0 = 32 * (ct & 1);
+                const int s = ct & 63, q0 = 32 * (ct >> 6);
                 const float4 xs = reinterpret_cast<const float4*>(bnd)[s];
                 uint32_t zv[32];
 #pragma unroll
@@ -400,28 +400,25 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                 if (lane == 0) mbar_arrive(bar_at(sm, B1_READY));
             }
             for (int n = 0; n < steps; ++n, ++v) {
-                // ---- epilogue 1a: D1[0] (main + cross terms) -> W_0 (even lanes), W_1 (odd lanes) into B2[0], B2[1]
-                const int q = 16 * sp + (lane >> 1), ip = lane & 1;
-                // W row of this lane from D1[h] (a_hi b_hi partial + cross terms), 32 columns at a time, split and
-                // written to B2[j] by the lanes with ip == j (tcgen05.ld is warp-collective: every lane loads)
-                auto write_w = [&](int h, int jmask) {
+                // ---- epilogue 1: D1[h] row m = q + 64 i' of this lane (m = 32 sp + lane) -> W_{2h+i'} into B2[i']:
+                // warps sp = 0, 1 own slice 2h, warps 2, 3 slice 2h + 1 (32 consecutive rows q per warp store)
+                const int q = 32 * (sp & 1) + lane, ip = sp >> 1;
+                auto write_w = [&](int h) {       // a_hi b_hi partial + cross terms, 32 columns at a time, split
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         uint32_t t0[32], t1[32];
                         tmem_ld32(tl + kD1 + 128 * h + 32 * hh, t0);
                         tmem_ld32(tl + kD1 + 128 * h + 64 + 32 * hh, t1);
                         tmem_wait_ld();
-                        if ((jmask >> ip) & 1) {
-                            float4 f[8];
+                        float4 f[8];
 #pragma unroll
-                            for (int c = 0; c < 8; ++c) {
-                                f[c].x = __uint_as_float(t0[4 * c]) + __uint_as_float(t1[4 * c]);
-                                f[c].y = __uint_as_float(t0[4 * c + 1]) + __uint_as_float(t1[4 * c + 1]);
-                                f[c].z = __uint_as_float(t0[4 * c + 2]) + __uint_as_float(t1[4 * c + 2]);
-                                f[c].w = __uint_as_float(t0[4 * c + 3]) + __uint_as_float(t1[4 * c + 3]);
-                            }
-                            write_b32(sm + kOffB2 + ip * 2 * kTile, q, 32 * hh, f);
+                        for (int c = 0; c < 8; ++c) {
+                            f[c].x = __uint_as_float(t0[4 * c]) + __uint_as_float(t1[4 * c]);
+                            f[c].y = __uint_as_float(t0[4 * c + 1]) + __uint_as_float(t1[4 * c + 1]);
+                            f[c].z = __uint_as_float(t0[4 * c + 2]) + __uint_as_float(t1[4 * c + 2]);
+                            f[c].w = __uint_as_float(t0[4 * c + 3]) + __uint_as_float(t1[4 * c + 3]);
                         }
+                        write_b32(sm + kOffB2 + ip * 2 * kTile, q, 32 * hh, f);
                     }
                 };
                 // GEMM-2 slice partials: lanes 0..15 accumulate K-chunk 0, lanes 16..31 K-chunk 1 of row 16 sp + lane % 16
@@ -447,31 +444,31 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                     if (lane == 0) mbar_arrive(bar_at(sm, D2P_EMPTY + j));
                 };
                 PW(14, mbar_wait(bar_at(sm, D1_FULL + 0), v & 1));
-                PW(15, mbar_wait(bar_at(sm, B2_FREE + 0), ((2 * v) & 1) ^ 1));
-                PW(15, mbar_wait(bar_at(sm, B2_FREE + 1), ((2 * v) & 1) ^ 1));
+                PW(15, mbar_wait(bar_at(sm, B2_FREE + ip), ((2 * v) & 1) ^ 1));
                 tc_fence_after();
-                write_w(0, 3);
+                write_w(0);
                 tc_fence_before();
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(bar_at(sm, D1_EMPTY + 0));
-                    mbar_arrive(bar_at(sm, B2_READY + 0));
-                    mbar_arrive(bar_at(sm, B2_READY + 1));
+                    mbar_arrive(bar_at(sm, B2_READY + ip));
                 }
                 // ---- epilogue 1b: D1[1] -> W_2 into B2[0] (after GEMM-2 slice 0), W_3 into B2[1] (after slice 1)
                 PW(16, mbar_wait(bar_at(sm, D1_FULL + 1), v & 1));
                 for (int j = 0; j < 2; ++j) {
                     PW(17, mbar_wait(bar_at(sm, B2_FREE + j), ((2 * v + 1) & 1) ^ 1));
                     add_slice(j);                                 // slice j is done (B2[j] is free)
-                    tc_fence_after();
-                    write_w(1, 1 << j);
-                    tc_fence_before();
-                    fence_proxy_async();
-                    __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(bar_at(sm, B2_READY + j));
-                        if (j == 1) mbar_arrive(bar_at(sm, D1_EMPTY + 1));
+                    if (ip == j) {
+                        tc_fence_after();
+                        write_w(1);
+                        tc_fence_before();
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) {
+                            mbar_arrive(bar_at(sm, B2_READY + j));
+                            mbar_arrive(bar_at(sm, D1_EMPTY + 1));
+                        }
                     }
                 }
                 add_slice(2);
@@ -583,10 +580,10 @@ cudaError_t launch_inner_r64tc(const InnerArgs& a, cudaStream_t s) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    {   // Y: (p: 64, i: 4 @ 256 B, q-row: rows @ 1024 B), box (32 p, 2 i, 64 q) -> SMEM rows i' + 2 q
-        const cuuint64_t dims[3] = {64, 4, rows};
-        const cuuint64_t strides[2] = {256, 1024};
-        const cuuint32_t box[3] = {32, 2, 64};
+    {   // Y: (p: 64, q-row: rows @ 1024 B, i: 4 @ 256 B), box (32 p, 64 q, 2 i) -> SMEM rows q + 64 i'
+        const cuuint64_t dims[3] = {64, rows, 4};
+        const cuuint64_t strides[2] = {1024, 256};
+        const cuuint32_t box[3] = {32, 64, 2};
         const cuuint32_t es[3] = {1, 1, 1};
         if (enc(&tmy, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a.y.cores), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
