@@ -1,8 +1,3 @@
-mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_contract.py -m gpu -q -p no:cacheprovider -x > gpurun_out/c3_pytest.log 2>&1
-timeout 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/c3_bench.json 2> gpurun_out/c3_bench.err
-if [ "$1" = "ncu" ]; then
-CMD="python bench.py --config C3 --steps 2 --warmup 1 --no-cpu --no-e2e"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:contract -s 1 -c 1 -o gpurun_out/c3_full -f $CMD > gpurun_out/c3_ncu.log 2>&1
-fi
-echo done
+O=gpurun_out
+CMD="python bench.py --config C3 --no-sub --no-cpu --no-e2e --steps 3 --warmup 3"
+$CMD > $O/c3.json 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:contract -s 2 -c 1 -o $O/c3_full -f $CMD > $O/ncu_c3.log 2>&1; echo "ncu rc=$?"
