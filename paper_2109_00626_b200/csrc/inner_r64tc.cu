@@ -477,20 +477,18 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                 uint32_t z0[32], z1[32];     // (slice 3 read above: every MMA of the step is complete)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
-                    z0[e] = __float_as_uint(zacc[e] + __shfl_down_sync(0xffffffffu, zacc[e], 16));
-                    z1[e] = __float_as_uint(zacc[32 + e] + __shfl_down_sync(0xffffffffu, zacc[32 + e], 16));
+                    z0[e] = __float_as_uint(zacc[e] + __shfl_xor_sync(0xffffffffu, zacc[e], 16));
+                    z1[e] = __float_as_uint(zacc[32 + e] + __shfl_xor_sync(0xffffffffu, zacc[32 + e], 16));
                 }
-                const int s = 16 * sp + lane;
+                // lanes t and t + 16 now both hold row 16 sp + t (chunk-0 + chunk-1 partial sums): lane t writes its
+                // columns 0..31, lane t + 16 columns 32..63 (the whole warp stores)
+                const int s = 16 * sp + (lane & 15);
                 if (n + 1 < steps) {
-                    if (lane < 16) {
-                        float4 f[8];
+                    const bool upper = lane >= 16;
+                    float4 f[8];
 #pragma unroll
-                        for (int c4 = 0; c4 < 8; ++c4) f[c4] = f4(z0 + 4 * c4);
-                        write_b32(b1, s, 0, f);
-#pragma unroll
-                        for (int c4 = 0; c4 < 8; ++c4) f[c4] = f4(z1 + 4 * c4);
-                        write_b32(b1, s, 32, f);
-                    }
+                    for (int c4 = 0; c4 < 8; ++c4) f[c4] = sel4(upper, f4(z1 + 4 * c4), f4(z0 + 4 * c4));
+                    write_b32(b1, s, upper ? 32 : 0, f);
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bar_at(sm, B1_READY));
