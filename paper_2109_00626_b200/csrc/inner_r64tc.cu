@@ -50,12 +50,13 @@ constexpr int kOffB1 = kOffB2 + 4 * kTile;        // Z as the GEMM-1 B operand
 constexpr int kOffBnd = kOffB1 + 2 * kTile;       // 2 buffers x {X_1, Y_1, X_N, Y_N} x 1 KB
 constexpr int kOffRed = kOffBnd + 2 * 4096;       // 4 floats: the final reduction
 constexpr int kOffBar = kOffRed + 64;
-constexpr int kNumBars = 32;
+constexpr int kNumBars = 36;
 constexpr int kSmemBytes = kOffBar + 8 * kNumBars + 16 + 1024;   // + TMEM address slot + alignment slack
 
 // barrier indices
-constexpr int FULL = 0, EMPTY = 4, LO_READY = 8, LO_FREE = 11, D1_FULL = 14, D1_EMPTY = 16, B2_READY = 18,
-              B2_FREE = 20, D2_FULL = 22, B1_READY = 23, BND_FULL = 24, BND_EMPTY = 26, D2P_FULL = 28, D2P_EMPTY = 30;
+constexpr int FULL = 0, EMPTY = 4, LO_READY = 8, LO_FREE = 12, D1_FULL = 16, D1_EMPTY = 18, B2_READY = 20,
+              B2_FREE = 22, D2_FULL = 24, B1_READY = 25, BND_FULL = 26, BND_EMPTY = 28, D2P_FULL = 30, D2P_EMPTY = 32;
+static_assert(kRaw <= 4 && kLo <= 4, "barrier slots");
 
 // TMEM columns (512 allocated).  The tensor core's accumulation into TMEM truncates (measured: -5.6e-8 relative per
 // accumulating MMA on positive sums, tools/tc05_probe.cu), so long chains are split: the large a_hi b_hi products
@@ -201,8 +202,8 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
     const int steps = N - 2;                      // interior steps per pair
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) { mbar_init(bar_at(sm, FULL + i), 1); mbar_init(bar_at(sm, EMPTY + i), 1); }
-        for (int i = 0; i < 3; ++i) { mbar_init(bar_at(sm, LO_READY + i), 2); mbar_init(bar_at(sm, LO_FREE + i), 1); }
+        for (int i = 0; i < kRaw; ++i) { mbar_init(bar_at(sm, FULL + i), 1); mbar_init(bar_at(sm, EMPTY + i), 1); }
+        for (int i = 0; i < kLo; ++i) { mbar_init(bar_at(sm, LO_READY + i), 2); mbar_init(bar_at(sm, LO_FREE + i), 1); }
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar_at(sm, D2P_FULL + i), 1); mbar_init(bar_at(sm, D2P_EMPTY + i), 4);
             mbar_init(bar_at(sm, D1_FULL + i), 1); mbar_init(bar_at(sm, D1_EMPTY + i), 4);
