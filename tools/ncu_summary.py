@@ -2,7 +2,7 @@
 """Summarise ncu output for profiles/: a launch list (our kernels vs input generation) and the key counters of a
 --set full capture.  Usage:
   python tools/ncu_summary.py launches <launches.csv> <out.txt>
-  python tools/ncu_summary.py full <report.ncu-rep> <out.txt> [traffic_key]
+  python tools/ncu_summary.py full <report.ncu-rep> <out.txt> [traffic_key pairs_per_launch]
 """
 import csv
 import json
@@ -11,7 +11,7 @@ import re
 import subprocess
 import sys
 
-OURS = re.compile(r"ttc::|inner_|contract_kernel|splice_kernel|reconstruct_kernel|ttsvd_kernel")
+OURS = re.compile(r"ttc::|inner_|contract_kernel|splice_kernel|reconstruct_kernel|ttsvd_")
 
 
 def short(name):
@@ -38,7 +38,7 @@ def launches(path, out):
     print("\n".join(lines[:3] + lines[-1:]))
 
 
-def full(rep, out, key=None):
+def full(rep, out, key=None, pairs=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -83,7 +83,8 @@ def full(rep, out, key=None):
         if key:
             tp = os.path.join(os.path.dirname(out), "traffic.json")
             tj = json.load(open(tp)) if os.path.exists(tp) else {}
-            tj[key] = rd + wr
+            tj[key] = {"bytes": rd + wr, "pairs": int(pairs) if pairs else None,
+                       "source": os.path.basename(out)}
             json.dump(tj, open(tp, "w"), indent=1)
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
@@ -93,4 +94,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None,
+             sys.argv[5] if len(sys.argv) > 5 else None)
