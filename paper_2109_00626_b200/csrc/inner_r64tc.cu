@@ -286,26 +286,22 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                     // ---- GEMM-1, halves h = 0, 1 (M = 128: rows i' + 2q)
                     for (int h = 0; h < 2; ++h) {
                         PW(3, mbar_wait(bar_at(sm, D1_EMPTY + h), (v & 1) ^ 1));
-                        uint32_t ar[2], al[2];
+                        const uint32_t d = tmem + kD1 + 128 * h;
                         for (int kc = 0; kc < 2; ++kc, ++k) {
                             PW(4, mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1));
                             PW(5, mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1));
-                            ar[kc] = sbase + kOffRaw + (k % kRaw) * kTile;
-                            al[kc] = sbase + kOffLo + (k % kLo) * kTile;
-                        }
-                        tc_fence_after();
-                        const uint32_t d = tmem + kD1 + 128 * h;
-                        for (int kc = 0; kc < 2; ++kc)
+                            tc_fence_after();
+                            const uint32_t ar = sbase + kOffRaw + (k % kRaw) * kTile;
+                            const uint32_t al = sbase + kOffLo + (k % kLo) * kTile;
                             for (int kk = 0; kk < 4; ++kk) {
-                                const uint64_t A = desc_sw128(ar[kc] + 32 * kk), Al = desc_sw128(al[kc] + 32 * kk);
+                                const uint64_t A = desc_sw128(ar + 32 * kk), Al = desc_sw128(al + 32 * kk);
                                 const uint64_t B = desc_sw128(b1 + 16384 * kc + 32 * kk);   // [Z_hi | Z_lo]
                                 mma_tf32(d, A, B, id1w, (kc | kk) ? 1u : 0u);             // a_hi [b_hi | b_lo]
                                 mma_tf32(d + 64, Al, B, id1, 1u);                         // + a_lo b_hi
                             }
-                        for (int kc = 0; kc < 2; ++kc) {
-                            const uint32_t kt = k - 2 + kc;
-                            mma_commit(bar_at(sm, EMPTY + kt % kRaw));
-                            mma_commit(bar_at(sm, LO_FREE + kt % kLo));
+                            // free this tile's raw slot and lo buffer as soon as its own MMAs are done
+                            mma_commit(bar_at(sm, EMPTY + k % kRaw));
+                            mma_commit(bar_at(sm, LO_FREE + k % kLo));
                         }
                         mma_commit(bar_at(sm, D1_FULL + h));
                     }

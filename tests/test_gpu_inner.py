@@ -325,3 +325,36 @@ def test_r64_tcgen05_kernel(monkeypatch, N, B):
         monkeypatch.delenv("TTC_KERNEL")
         for b in range(B):
             assert abs(got[b] - ref[b]) <= 2e-5 * abs(ref[b]), (kind, b, got[b], ref[b])
+
+
+def test_graph_replay_and_concurrent_streams_are_reentrant():
+    """No kernel keeps global state (ttc.h: re-entrant): ttc_inner captured in a CUDA graph and replayed gives the
+    eager result bitwise, and the C5 kernel (formerly handing out pairs from global ticket counters) run on two
+    streams at once, twice over, gives bitwise the single-stream result for both batches."""
+    X, Y = ttgen.config_batch("C1", kind="corr")
+    XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+    eager = ttc.ttc_inner(XD, YD).clone()
+    s = torch.cuda.Stream()
+    out = torch.empty_like(eager)
+    with torch.cuda.stream(s):
+        ttc.ttc_inner(XD, YD, out=out, stream=s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ttc.ttc_inner(XD, YD, out=out, stream=s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    batches = [ttgen.config_batch("C5", kind="corr", b0=b0, B=300, device=DEV) for b0 in (0, 300)]
+    devs = [(ttc.TTDevice.from_batch(Xb), ttc.TTDevice.from_batch(Yb)) for Xb, Yb in batches]
+    ref = [ttc.ttc_inner(xd, yd).clone() for xd, yd in devs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.full((300,), float("nan"), device=DEV) for _ in range(2)]
+    for rep in range(2):
+        for k in range(2):
+            ttc.ttc_inner(devs[k][0], devs[k][1], out=outs[k], stream=streams[k])
+        torch.cuda.synchronize()
+        for k in range(2):
+            assert torch.equal(outs[k], ref[k]), (rep, k)
