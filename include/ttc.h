@@ -165,12 +165,22 @@ void ttc_contract_plan_destroy(ttc_contract_plan* plan);
  * plan's out_perm to obtain Eq. 8's order), NULL = identity.  out_dev: device fp32, prod_n I_n floats per train
  * at out_offsets_dev[b] (device int64 [B]; NULL = packed, train b at b * prod_n I_n).
  * The kernel splits every train into a left and a right block of modes whose partial products fit in shared
- * memory together (prod_{n<=k} I_n R_k + R_k prod_{n>k} I_n <= 48K floats for some k) and multiplies them;
- * trains with no such split return TTC_ERR_UNSUPPORTED.  Errors as ttc_inner (TTC_ERR_MODES for a perm that is
- * not a permutation of 1..N).
+ * memory together (prod_{n<=k} I_n R_k + R_k prod_{n>k} I_n <= 48K floats for some k) and multiplies them in one
+ * launch (one CTA per train).  Trains with no such split (Example 2's outputs) need
+ * ttc_reconstruct_ws: ttc_reconstruct returns TTC_ERR_ARG for them, naming the workspace size.  Errors as
+ * ttc_inner (TTC_ERR_MODES for a perm that is not a permutation of 1..N).
+ * ttc_reconstruct_workspace: bytes of device workspace ttc_reconstruct_ws needs for this batch and perm (0: the
+ *   shared-memory kernel runs; else B x the two partial-product chains' ping-pong buffers).  Host only.
+ * ttc_reconstruct_ws: ttc_reconstruct with a caller-owned device workspace (16-byte aligned, >= that size; NULL /
+ *   0 when it is 0).  The large path is a chain of tiled FP32 GEMM launches on `stream` -- Left = X_1..X_k and
+ *   Right = X_{k+1}..X_N built in the workspace, k minimising the multiply-adds -- with the output tile stored
+ *   through the permuted Eq. 2 strides.  Same result as the one-launch kernel to fp32 rounding.
  * ------------------------------------------------------------------------------------------------- */
 ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
                            void* stream);
+ttc_status ttc_reconstruct_workspace(const ttc_tt_batch* t, const int32_t* perm, int64_t* workspace_bytes);
+ttc_status ttc_reconstruct_ws(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
+                              void* workspace_dev, int64_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------------
  * ttc_tt_svd: TT decomposition of a batch of dense tensors (Alg. 1, TT-SVD), optionally of the
@@ -189,8 +199,11 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
  *   a pipeline of 1 + 2 (N - 1) launches (one warp per eigenproblem); with NULL / too small a workspace, or
  *   larger sides, as one fused launch (one CTA per tensor).  Both give the same ranks and cores to fp32
  *   rounding.  The library allocates nothing.
- * The tensor is held in shared memory: prod(dims) <= 16384 and every unfolding's smaller side <= 64 (else
- * TTC_ERR_UNSUPPORTED).  eps < 0: TTC_ERR_ARG.
+ * Tensors of prod(dims) <= 16384 with every unfolding's smaller side <= 64 are held in shared memory (the two
+ * paths above).  Larger ones (Example 2's 20 x 20 x 20 x 5 and 20 x 20 x 20 x 5 x 4) take a
+ * one-sided Jacobi kernel over the workspace, which is then REQUIRED (8 (2 prod(dims) + gmax^2 + 16) bytes per
+ * tensor, gmax the largest smaller side; NULL / too small: TTC_ERR_ARG naming the size); limits prod(dims) <= 2^27
+ * and gmax <= 1024 (else TTC_ERR_UNSUPPORTED).  eps < 0: TTC_ERR_ARG.
  * ------------------------------------------------------------------------------------------------- */
 ttc_status ttc_tt_svd_capacity(int32_t order, const int32_t* dims, const int32_t* perm, int64_t* train_cap);
 ttc_status ttc_tt_svd_workspace(int32_t batch, int32_t order, const int32_t* dims, const int32_t* perm,

@@ -34,8 +34,8 @@ TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG 
 TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
 
 EXPORTED = ("ttc_inner", "ttc_inner_ordered", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
-            "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity", "ttc_tt_svd_workspace",
-            "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
+            "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_reconstruct_workspace", "ttc_reconstruct_ws",
+            "ttc_tt_svd", "ttc_tt_svd_capacity", "ttc_tt_svd_workspace", "ttc_contract", "ttc_contract_plan_destroy", "ttc_pair_cost", "ttc_partition", "ttc_status_string",
             "ttc_last_error", "ttc_version")
 
 
@@ -67,6 +67,9 @@ _lib.ttc_status_string.argtypes = [ctypes.c_int]
 _lib.ttc_last_error.restype = ctypes.c_char_p
 _lib.ttc_version.restype = ctypes.c_int32
 _lib.ttc_reconstruct.argtypes = [_P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_reconstruct_workspace.argtypes = [_P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p]
+_lib.ttc_reconstruct_ws.argtypes = [_P(ttc_tt_batch), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
 _lib.ttc_tt_svd_capacity.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 _lib.ttc_tt_svd_workspace.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_void_p]
@@ -74,8 +77,8 @@ _lib.ttc_tt_svd.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, cty
                             ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                             ctypes.c_void_p]
 for _f in ("ttc_inner", "ttc_inner_ordered", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
-           "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_tt_svd", "ttc_tt_svd_capacity",
-           "ttc_tt_svd_workspace", "ttc_contract", "ttc_pair_cost", "ttc_partition"):
+           "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_reconstruct_workspace", "ttc_reconstruct_ws",
+           "ttc_tt_svd", "ttc_tt_svd_capacity", "ttc_tt_svd_workspace", "ttc_contract", "ttc_pair_cost", "ttc_partition"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -306,15 +309,33 @@ def ttc_contract(plan: ContractPlan, x: TTDevice, y: TTDevice, out: torch.Tensor
     return out, plan.ranks, plan.offsets
 
 
-def ttc_reconstruct(t: TTDevice, perm=None, out: torch.Tensor = None, out_offsets=None, stream=None) -> torch.Tensor:
-    """Dense tensor of every train (ttc.h: ttc_reconstruct), Eq. 2 order after the optional mode permutation
-    perm (1-based; e.g. a contraction plan's perm gives Eq. 8's order).  Returns float32 [B * prod(dims)] (packed)."""
+def ttc_reconstruct_workspace(t: TTDevice, perm=None) -> int:
+    """Bytes of device workspace ttc_reconstruct_ws needs (0: the one-launch shared-memory kernel runs)."""
+    pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    nb = ctypes.c_int64(0)
+    _check(_lib.ttc_reconstruct_workspace(ctypes.byref(t.c), _ptr(pm), ctypes.byref(nb)))
+    return nb.value
+
+
+def ttc_reconstruct(t: TTDevice, perm=None, out: torch.Tensor = None, out_offsets=None, stream=None,
+                    workspace: torch.Tensor = None) -> torch.Tensor:
+    """Dense tensor of every train (ttc.h: ttc_reconstruct / ttc_reconstruct_ws), Eq. 2 order after the optional
+    mode permutation perm (1-based; e.g. a contraction plan's perm gives Eq. 8's order).  Returns float32
+    [B * prod(dims)] (packed).  workspace: uint8 device scratch of ttc_reconstruct_workspace bytes for trains
+    beyond shared memory (allocated here from torch's caching allocator when None and needed)."""
     n_el = int(np.prod(t.dims_np.astype(np.int64))) if t.N else 1
     if out is None:
         out = torch.empty(max(t.B * n_el, 0), dtype=torch.float32, device=t.cores.device)
     pm = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
-    _check(_lib.ttc_reconstruct(ctypes.byref(t.c), _ptr(pm), _ptr(out) if out.numel() else None, _ptr(out_offsets),
-                                _stream_handle(stream)))
+    ws = workspace
+    if ws is None:
+        nb = ttc_reconstruct_workspace(t, pm)
+        ws = torch.empty(nb, dtype=torch.uint8, device=t.cores.device) if nb else None
+    _check(_lib.ttc_reconstruct_ws(ctypes.byref(t.c), _ptr(pm), _ptr(out) if out.numel() else None, _ptr(out_offsets),
+                                   _ptr(ws) if ws is not None else None, int(ws.numel()) if ws is not None else 0,
+                                   _stream_handle(stream)))
+    if workspace is None:
+        _keep_alive(stream, t.cores.device, ws)
     return out
 
 

@@ -311,9 +311,57 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
 }
 }  // namespace
 
-ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
-                           void* stream) {
+namespace {
+
+// The large path (reconstruct_big.cu): the split k minimising the batch's multiply-adds (chain steps + the final
+// product), the tiles of every launch, and the ping-pong buffers' floats (each rounded to 16 bytes).
+ttc_status recon_big_plan(const HostTrain& h, const ttc_tt_batch* t, ttc::ReconBigArgs* a) {
+    const int N = t->order, B = t->batch;
+    a->B = B; a->N = N;
+    a->pre[0] = 1;
+    for (int n = 0; n < N; ++n) a->pre[n + 1] = a->pre[n] * t->dims[n];
+    a->suf[N] = 1;
+    for (int n = N - 1; n >= 0; --n) a->suf[n] = a->suf[n + 1] * t->dims[n];
+    for (int n = 0; n < N; ++n) a->dims[n] = t->dims[n];
+    auto tiles = [](int64_t m, int64_t n) { return ((m + 63) / 64) * ((n + 63) / 64); };
+    double best = -1.0;
+    for (int k = 1; k < N; ++k) {
+        double mac = 0.0;
+        for (int b = 0; b < B; ++b) {
+            for (int j = 1; j < k; ++j) mac += (double)a->pre[j] * h.rank(b, j) * t->dims[j] * h.rank(b, j + 1);
+            for (int j = k; j < N - 1; ++j)
+                mac += (double)h.rank(b, j) * t->dims[j] * h.rank(b, j + 1) * a->suf[j + 1];
+            mac += (double)a->pre[k] * h.rank(b, k) * a->suf[k];
+        }
+        if (best < 0.0 || mac < best) { best = mac; a->k = k; }
+    }
+    const int k = a->k;
+    int64_t wl = 0, wr = 0;
+    for (int j = 0; j < TTC_MAX_ORDER; ++j) a->tiles_left[j] = a->tiles_right[j] = 0;
+    a->tiles_final = 0;
+    for (int b = 0; b < B; ++b) {
+        for (int j = 1; j < k; ++j) {
+            wl = std::max(wl, a->pre[j + 1] * h.rank(b, j + 1));
+            a->tiles_left[j] = std::max(a->tiles_left[j], tiles(a->pre[j], (int64_t)t->dims[j] * h.rank(b, j + 1)));
+        }
+        for (int j = k; j < N - 1; ++j) {
+            wr = std::max(wr, (int64_t)h.rank(b, j) * a->suf[j]);
+            a->tiles_right[j] = std::max(a->tiles_right[j], tiles((int64_t)h.rank(b, j) * t->dims[j], a->suf[j + 1]));
+        }
+        a->tiles_final = std::max(a->tiles_final, tiles(a->pre[k], a->suf[k]));
+    }
+    a->ws_left = (wl + 3) & ~int64_t(3);
+    a->ws_right = (wr + 3) & ~int64_t(3);
+    if (a->tiles_final > 0x7fffffffLL) return fail(TTC_ERR_UNSUPPORTED, "output of %lld x %lld per train too large",
+                                                    (long long)a->pre[k], (long long)a->suf[k]);
+    return TTC_OK;
+}
+
+// ttc_reconstruct_ws, or (query != NULL) only the workspace it needs
+ttc_status reconstruct_impl(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
+                            void* workspace_dev, int64_t workspace_bytes, void* stream, int64_t* query) {
     g_last_error.clear();
+    if (query) *query = 0;
     HostTrain h;
     ttc_status st;
     if ((st = check_batch(t, "T", TTC_MAX_ORDER, &h)) != TTC_OK) return st;
@@ -337,8 +385,10 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
     int64_t pair_elems = 1;
     for (int n = 0; n < N; ++n) pair_elems *= t->dims[n];
     if (B == 0) return TTC_OK;
-    if (!out_dev) return fail(TTC_ERR_NULL, "out_dev is NULL");
-    if (reinterpret_cast<uintptr_t>(out_dev) & 3u) return fail(TTC_ERR_ALIGN, "out_dev not 4-byte aligned");
+    if (!query) {
+        if (!out_dev) return fail(TTC_ERR_NULL, "out_dev is NULL");
+        if (reinterpret_cast<uintptr_t>(out_dev) & 3u) return fail(TTC_ERR_ALIGN, "out_dev not 4-byte aligned");
+    }
     // the split k: left block modes 1..k, right block k+1..N; shared memory = both blocks + build temporaries +
     // the row / column offset tables, the batch maximum over pairs, minimised over k
     const int64_t kSmemMax = 220 * 1024;
@@ -374,8 +424,36 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
             best_k = k; best = bytes; bl = lb; bt1 = t1; br = rb; bt2 = t2;
         }
     }
-    if (best_k < 0)
-        return fail(TTC_ERR_UNSUPPORTED, "no split of the %d modes fits shared memory (partial products too large)", N);
+    // TTC_RECON_BIG=1 forces the workspace path (tests compare it with the shared-memory kernel)
+    if (N == 1 && best_k < 0)
+        return fail(TTC_ERR_UNSUPPORTED, "order-1 train of %d entries exceeds shared memory", t->dims[0]);
+    if (best_k < 0 || (N > 1 && std::getenv("TTC_RECON_BIG"))) {
+        ttc::ReconBigArgs a;
+        std::memset(&a, 0, sizeof(a));
+        ttc_status st2;
+        if ((st2 = recon_big_plan(h, t, &a)) != TTC_OK) return st2;
+        const int64_t need = 4 * (int64_t)B * (2 * a.ws_left + 2 * a.ws_right);
+        if (query) {
+            *query = need;
+            return TTC_OK;
+        }
+        if (need > 0 && (!workspace_dev || workspace_bytes < need))
+            return fail(TTC_ERR_ARG, "no split of the %d modes fits shared memory: the workspace path needs %lld bytes "
+                        "(ttc_reconstruct_workspace), got %lld", N, (long long)need, (long long)workspace_bytes);
+        if (reinterpret_cast<uintptr_t>(workspace_dev) & 15u) return fail(TTC_ERR_ALIGN, "workspace_dev not 16-byte aligned");
+        a.row_fast = 0;
+        for (int n = 0; n < a.k; ++n) a.row_fast |= ostride[n] == 1;
+        for (int n = 0; n < N; ++n) a.ostride[n] = ostride[n];
+        a.t = to_dev(h);
+        a.out = out_dev;
+        a.out_offsets = out_offsets_dev;
+        a.pair_elems = pair_elems;
+        a.ws = static_cast<float*>(workspace_dev);
+        const cudaError_t e = ttc::launch_reconstruct_big(a, reinterpret_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return cuda_fail(e, "ttc_reconstruct launch");
+        return TTC_OK;
+    }
+    if (query) return TTC_OK;
     ttc::ReconArgs a;
     std::memset(&a, 0, sizeof(a));
     a.B = B; a.N = N; a.k = best_k;
@@ -399,6 +477,23 @@ ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* ou
     const cudaError_t e = ttc::launch_reconstruct(a, (size_t)best, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "ttc_reconstruct launch");
     return TTC_OK;
+}
+
+}  // namespace
+
+ttc_status ttc_reconstruct(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
+                           void* stream) {
+    return reconstruct_impl(t, perm, out_dev, out_offsets_dev, nullptr, 0, stream, nullptr);
+}
+
+ttc_status ttc_reconstruct_workspace(const ttc_tt_batch* t, const int32_t* perm, int64_t* workspace_bytes) {
+    if (!workspace_bytes) return fail(TTC_ERR_NULL, "workspace_bytes is NULL");
+    return reconstruct_impl(t, perm, nullptr, nullptr, nullptr, 0, nullptr, workspace_bytes);
+}
+
+ttc_status ttc_reconstruct_ws(const ttc_tt_batch* t, const int32_t* perm, float* out_dev, const int64_t* out_offsets_dev,
+                              void* workspace_dev, int64_t workspace_bytes, void* stream) {
+    return reconstruct_impl(t, perm, out_dev, out_offsets_dev, workspace_dev, workspace_bytes, stream, nullptr);
 }
 
 namespace {
@@ -442,11 +537,18 @@ ttc_status ttsvd_shape(int32_t order, const int32_t* dims, const int32_t* perm, 
     }
     *cap = c;
     *gmax = (int32_t)g;
-    if (total > 16384)
-        return fail(TTC_ERR_UNSUPPORTED, "tensor of %lld elements: the TT-SVD kernel holds <= 16384 in shared memory",
-                    (long long)total);
-    if (g > 64) return fail(TTC_ERR_UNSUPPORTED, "an unfolding's smaller side is %lld > 64", (long long)g);
+    // beyond the shared-memory kernels (16,384 elements, Gram side 64) the workspace-based one-sided Jacobi kernel
+    // (ttsvd_big.cu) takes over, up to a side of kTtsvdBigMaxSide and 2^27 elements
+    if (total > (int64_t(1) << 27))
+        return fail(TTC_ERR_UNSUPPORTED, "tensor of %lld elements (> 2^27)", (long long)total);
+    if (g > ttc::kTtsvdBigMaxSide)
+        return fail(TTC_ERR_UNSUPPORTED, "an unfolding's smaller side is %lld > %d", (long long)g, ttc::kTtsvdBigMaxSide);
     return TTC_OK;
+}
+
+// TTC_TTSVD_BIG=1 forces the workspace kernel for every size (tests compare it with the shared-memory kernels)
+bool ttsvd_needs_big(int64_t total, int32_t gmax) {
+    return total > 16384 || gmax > 64 || std::getenv("TTC_TTSVD_BIG") != nullptr;
 }
 
 }  // namespace
@@ -485,6 +587,10 @@ ttc_status ttc_tt_svd_workspace(int32_t batch, int32_t order, const int32_t* dim
     if ((s = ttsvd_shape(order, dims, perm, &rd, &st, &cap, &gmax)) != TTC_OK) return s;
     int64_t total = 1, off[6];
     for (int n = 0; n < order; ++n) total *= rd[n];
+    if (ttsvd_needs_big(total, gmax)) {
+        *workspace_bytes = 8 * (int64_t)batch * ttc::ttsvd_big_ws_per((int32_t)total, gmax);
+        return TTC_OK;
+    }
     *workspace_bytes = (order >= 2 && gmax <= 32) ? ttsvd_ws_layout(batch, total, gmax, off) : 0;
     return TTC_OK;
 }
@@ -519,6 +625,17 @@ ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const f
     a.ranks = ranks_dev;
     const int64_t g = gmax;
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (ttsvd_needs_big(total, gmax)) {   // one-sided Jacobi over the caller's fp64 workspace (ttsvd_big.cu)
+        const int64_t need = 8 * (int64_t)batch * ttc::ttsvd_big_ws_per((int32_t)total, gmax);
+        if (!workspace_dev || workspace_bytes < need)
+            return fail(TTC_ERR_ARG, "tensors of %lld elements (largest unfolding side %d) need a workspace of %lld bytes "
+                        "(ttc_tt_svd_workspace), got %lld", (long long)total, gmax, (long long)need,
+                        (long long)workspace_bytes);
+        if (reinterpret_cast<uintptr_t>(workspace_dev) & 7u) return fail(TTC_ERR_ALIGN, "workspace_dev not 8-byte aligned");
+        const cudaError_t e = ttc::launch_ttsvd_big(a, static_cast<double*>(workspace_dev), cs);
+        if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd launch");
+        return TTC_OK;
+    }
     int64_t off[6];
     const int64_t need = (order >= 2 && gmax <= 32) ? ttsvd_ws_layout(batch, total, g, off) : 0;
     if (need > 0 && workspace_dev && workspace_bytes >= need && !std::getenv("TTC_TTSVD_FUSED")) {

@@ -122,6 +122,24 @@ struct ReconArgs {
 };
 cudaError_t launch_reconstruct(const ReconArgs& a, size_t smem_bytes, cudaStream_t s);
 
+// trains whose partial products exceed shared memory (reconstruct_big.cu): a chain of tiled GEMM launches over a
+// caller-owned workspace (0-based modes; pre[j] = prod_{n<j} I_n, suf[j] = prod_{n>=j} I_n)
+struct ReconBigArgs {
+    int32_t  B, N, k;                   // split: Left = cores 0..k-1, Right = cores k..N-1 (1 <= k < N)
+    int32_t  row_fast;                  // 1: the output's stride-1 mode is one of Left's (store along rows)
+    int32_t  dims[TTC_MAX_ORDER];
+    int64_t  pre[TTC_MAX_ORDER + 1], suf[TTC_MAX_ORDER + 1];
+    int64_t  ostride[TTC_MAX_ORDER];
+    int64_t  tiles_left[TTC_MAX_ORDER], tiles_right[TTC_MAX_ORDER], tiles_final;   // 64 x 64 tiles per launch
+    TrainDev t;
+    float*   out;
+    const int64_t* out_offsets;
+    int64_t  pair_elems;
+    float*   ws;                        // B x (2 ws_left + 2 ws_right) floats
+    int64_t  ws_left, ws_right;         // floats of one Left / Right ping-pong buffer
+};
+cudaError_t launch_reconstruct_big(const ReconBigArgs& a, cudaStream_t s);
+
 // ---- batched TT-SVD (ttsvd.cu) -------------------------------------------------------------------------
 struct TtsvdArgs {
     int32_t  B, N, elems, gmax;         // tensors, order, prod dims (<= shared memory), largest Gram side
@@ -144,5 +162,10 @@ struct TtsvdWs {
     double*  nrm;                       // B
 };
 cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStream_t s);
+// tensors beyond the shared-memory kernels (ttsvd_big.cu): one CTA per tensor over an fp64 workspace of
+// ttsvd_big_ws_per(elems, gmax) doubles per tensor; every unfolding's smaller side <= kTtsvdBigMaxSide
+constexpr int kTtsvdBigMaxSide = 1024;
+int64_t     ttsvd_big_ws_per(int32_t elems, int32_t gmax);
+cudaError_t launch_ttsvd_big(const TtsvdArgs& a, double* ws, cudaStream_t s);
 
 }  // namespace ttc

@@ -28,7 +28,7 @@ def _declared_symbols():
 
 def test_library_exports_every_declared_symbol():
     syms = _declared_symbols()
-    assert len(syms) == 17
+    assert len(syms) == 19
     lib = ctypes.CDLL(ttc.LIB_PATH)
     for s in syms:
         assert hasattr(lib, s), s
@@ -289,6 +289,15 @@ def test_tt_svd_workspace_sizes():
     assert ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(2, 1)) > 0
     with pytest.raises(ttc.TTCError):
         ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(1, 1))
+    # beyond shared memory (Example 2's (ii) / (iii)): the one-sided Jacobi kernel's fp64 Z, A (prod(dims) each)
+    # and V (gmax^2) per tensor, gmax = the largest smaller side of an unfolding (400 x 100 -> 100; 400 x 400 -> 400)
+    assert ttc.ttc_tt_svd_workspace(B, (20, 20, 20, 5)) == 8 * B * (2 * 40000 + 100 * 100 + 16)
+    assert ttc.ttc_tt_svd_workspace(B, (20, 20, 20, 5, 4)) == 8 * B * (2 * 160000 + 400 * 400 + 16)
+    assert ttc.ttc_tt_svd_workspace(B, (5, 20, 20, 20), perm=(2, 3, 4, 1)) == 8 * B * (2 * 40000 + 100 * 100 + 16)
+    assert ttc.ttc_tt_svd_workspace(B, (70, 70)) == 8 * B * (2 * 4900 + 70 * 70 + 16)   # side 70 > 64
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_tt_svd_workspace(B, (2000, 2000))            # smaller side 2000 > 1024
+    assert e.value.status == ttc.TTC_ERR_UNSUPPORTED
 
 
 def test_inner_ordered_validates_the_permutation():
@@ -345,3 +354,20 @@ def test_tt_svd_dense_size_overflow_is_detected():
     assert ttc._lib.ttc_tt_svd_capacity(3, d.ctypes.data, None, ctypes.byref(cap)) == ttc.TTC_ERR_OVERFLOW
     d = np.array([1 << 15, 1 << 15, 1 << 15], np.int32)   # 2^45 > 2^40
     assert ttc._lib.ttc_tt_svd_capacity(3, d.ctypes.data, None, ctypes.byref(cap)) == ttc.TTC_ERR_OVERFLOW
+
+
+def test_reconstruct_workspace_sizes():
+    """Host-only sizing of ttc_reconstruct_ws's workspace: 0 where a shared-memory split exists; else B x two
+    ping-pong buffers per chain, the split k minimising the multiply-adds (ties: the smaller k).  Hand values for
+    dims (7, 2000, 9), ranks (1, 7, 9, 1): k = 1 and k = 2 both cost 2,016,000 MACs, k = 1 has no left chain and
+    one right step, Q_1 = R_1 x I_2 I_3 = 7 x 18,000 floats per buffer."""
+    r = np.tile(np.array([1, 7, 9, 1], np.int32), (3, 1))
+    T = ttgen.gaussian_batch(1, 0, 0, 0, r, (7, 2000, 9), "geo")
+    TD = ttc.TTDevice.from_batch(T, "cpu")
+    assert ttc.ttc_reconstruct_workspace(TD) == 4 * 3 * 2 * 7 * 18000
+    assert ttc.ttc_reconstruct_workspace(TD, [3, 1, 2]) == 4 * 3 * 2 * 7 * 18000   # perm: output strides only
+    small = ttgen.gaussian_batch(2, 0, 0, 0, np.tile(np.array([1, 3, 3, 1], np.int32), (2, 1)), (4, 5, 6), "geo")
+    assert ttc.ttc_reconstruct_workspace(ttc.TTDevice.from_batch(small, "cpu")) == 0
+    with pytest.raises(ttc.TTCError) as e:
+        ttc.ttc_reconstruct_workspace(TD, [1, 1, 2])
+    assert e.value.status == ttc.TTC_ERR_MODES

@@ -1,6 +1,8 @@
 """GPU parity for ttc_reconstruct (dense tensors of trains, Alg. 2 steps 5-6) against the
 oracle's Eq. 9 reconstruction (O1a, pinned in test_oracle_dense.py) and numpy's transpose for the permutation;
 end to end, contraction / splice on the GPU followed by reconstruction equals the dense Eq. 8 definition."""
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -39,9 +41,13 @@ def _check(T, got, perm=None, tol=2e-6):
         assert np.max(np.abs(seg - want) / np.maximum(bound, 1e-30)) <= tol, f"train {b}"
 
 
+@pytest.mark.parametrize("big", [False, True])
 @pytest.mark.parametrize("case", range(7))
-def test_random_trains(case):
-    """Orders 1..6, odd mode sizes, heterogeneous per-train ranks, with and without a permutation."""
+def test_random_trains(case, big, monkeypatch):
+    """Orders 1..6, odd mode sizes, heterogeneous per-train ranks, with and without a permutation; through the
+    one-launch shared-memory kernel and (TTC_RECON_BIG=1) the workspace GEMM chain of reconstruct_big.cu."""
+    if big:
+        monkeypatch.setenv("TTC_RECON_BIG", "1")
     rng = np.random.default_rng(40 + case)
     dims = [(7,), (3, 5), (4, 1, 6), (2, 3, 4, 5), (5, 4, 3, 2, 3), (3, 2, 3, 2, 3, 2), (20, 20, 20, 20)][case]
     N = len(dims)
@@ -106,6 +112,28 @@ def test_splice_then_reconstruct_is_eq8():
         got = dense[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
         err = np.linalg.norm(got - want) / oracle.normaliser(X.train(b), Y.train(b))
         assert err <= 1e-5
+
+
+@pytest.mark.parametrize("dims,rk", [((20, 20, 5, 20, 20, 5), (1, 5, 100, 20, 100, 5, 1)),
+                                     ((5, 20, 20, 20, 5), (1, 5, 100, 100, 5, 1)),
+                                     ((7, 2000, 9), (1, 7, 9, 1))])
+def test_beyond_shared_memory(dims, rk):
+    """Trains whose partial products fit no shared-memory split (Example 2 case (ii)'s TTCP output, 4,000,000
+    entries with ranks 100; an order-5 one with two rank-100 bonds; a long middle mode): the workspace path,
+    heterogeneous per-train ranks, identity and random permutations."""
+    rng = np.random.default_rng(sum(dims))
+    B = 2
+    r = np.tile(np.array(rk, np.int32), (B, 1))
+    r[1, 1:-1] = np.maximum(1, r[1, 1:-1] - 1)
+    T = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, r, dims, "geo")
+    TD = ttc.TTDevice.from_batch(T, DEV)
+    assert ttc.ttc_reconstruct_workspace(TD) > 0
+    with pytest.raises(ttc.TTCError) as e:   # the workspace-free entry point names the size it needs
+        ttc._check(ttc._lib.ttc_reconstruct(ctypes.byref(TD.c), None, ttc._ptr(torch.empty(1, device=DEV)), None, None))
+    assert e.value.status == ttc.TTC_ERR_ARG and "workspace" in str(e.value)
+    _check(T, _recon(T))
+    perm = list(rng.permutation(len(dims)) + 1)
+    _check(T, _recon(T, perm), perm)
 
 
 def test_reconstruct_errors():

@@ -117,7 +117,7 @@ def test_alg2_pipeline_on_gpu(shape_x, shape_y, n, m):
 
 def test_ttsvd_errors():
     with pytest.raises(ttc.TTCError) as e:
-        ttc.ttc_tt_svd_capacity((30, 30, 30))           # 27,000 elements > 16,384
+        ttc.ttc_tt_svd_capacity((2000, 2000))           # unfolding side 2000 > 1024
     assert e.value.status == ttc.TTC_ERR_UNSUPPORTED
     with pytest.raises(ttc.TTCError) as e:
         ttc.ttc_tt_svd_capacity((4, 5), perm=[1, 1])
@@ -125,17 +125,18 @@ def test_ttsvd_errors():
 
 
 @pytest.mark.parametrize("dims,eps", [((3, 4, 5), 0.0), ((20, 20, 20), 0.0), ((6, 5, 7, 4), 0.2), ((2, 3, 4, 3, 2), 0.1)])
-def test_pipeline_matches_fused_kernel(dims, eps, monkeypatch):
-    """The launch pipeline (one-warp Jacobi per eigenproblem, Gram sides <= 32) and the fused one-CTA-per-tensor
-    kernel (TTC_TTSVD_FUSED=1) implement the same Alg. 1 with the same readings: equal ranks, cores equal to
-    fp32 rounding (both stop Jacobi at the same rotation threshold; rotation order differs)."""
+@pytest.mark.parametrize("other", ["TTC_TTSVD_FUSED", "TTC_TTSVD_BIG"])
+def test_pipeline_matches_fused_kernel(dims, eps, other, monkeypatch):
+    """The launch pipeline (one-warp Jacobi per eigenproblem, Gram sides <= 32), the fused one-CTA-per-tensor
+    kernel (TTC_TTSVD_FUSED=1) and the one-sided Jacobi kernel of the large path (TTC_TTSVD_BIG=1) implement the
+    same Alg. 1 with the same readings: equal ranks, cores equal to fp32 rounding (rotation orders differ)."""
     rng = np.random.default_rng(len(dims) + int(10 * eps))
     Xs = [rng.standard_normal(dims) for _ in range(5)]
     dense = _dense_batch(Xs)
     T_pipe = ttc.ttc_tt_svd(dense, dims, eps)
-    monkeypatch.setenv("TTC_TTSVD_FUSED", "1")
+    monkeypatch.setenv(other, "1")        # the fused kernel, or the workspace one-sided Jacobi kernel
     T_fused = ttc.ttc_tt_svd(dense, dims, eps)
-    monkeypatch.delenv("TTC_TTSVD_FUSED")
+    monkeypatch.delenv(other)
     for b, (cp, cf) in enumerate(zip(_trains(T_pipe), _trains(T_fused))):
         assert [c.shape for c in cp] == [c.shape for c in cf], f"tensor {b}: ranks differ"
         scale = np.linalg.norm(Xs[b])
@@ -160,3 +161,79 @@ def test_sigma_floor_on_constructed_spectra(spectrum, want):
         assert [c.shape for c in cs] == [c.shape for c in want_cores]
         err = np.linalg.norm(ref.dense_from_tt(cs) - X32) / np.linalg.norm(X32)
         assert err <= 2e-5
+
+
+EXAMPLE2 = [(20, 20, 20, 5), (20, 20, 20, 5, 4)]   # PAPER.md:406-412, cases (ii) and (iii)
+
+
+@pytest.mark.parametrize("dims", EXAMPLE2)
+def test_example2_sizes_match_oracle(dims):
+    """Example 2's order-4 and order-5 Gaussian tensors (40,000 / 160,000 elements; unfoldings up to 400 x 100 and
+    400 x 400) through the workspace kernel: the ranks of O6 (full: [1, 20, 100, 5, 1] / [1, 20, 400, 20, 4, 1]),
+    cores entry by entry (R24 signs), reconstruction and left-orthonormality."""
+    rng = np.random.default_rng(len(dims))
+    Xs = [rng.standard_normal(dims).astype(np.float32).astype(np.float64) for _ in range(2)]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 0.0)
+    for b, cs in enumerate(_trains(T)):
+        want = ttsvd.tt_svd(Xs[b], 0.0)
+        assert [c.shape for c in cs] == [w.shape for w in want], f"tensor {b}: ranks differ"
+        for n, (c, w) in enumerate(zip(cs, want)):
+            d = np.max(np.abs(c - w))
+            assert d <= 1e-5 * max(1.0, np.max(np.abs(w))), f"tensor {b} core {n + 1}: max |diff| {d:.3e}"
+        err = np.linalg.norm(ref.dense_from_tt(cs) - Xs[b]) / np.linalg.norm(Xs[b])
+        assert err <= 2e-6, f"tensor {b}: relative reconstruction error {err:.3e}"
+        for c in cs[:-1]:
+            U = c.reshape(-1, c.shape[2], order="F")
+            np.testing.assert_allclose(U.T @ U, np.eye(U.shape[1]), atol=1e-5)
+
+
+@pytest.mark.parametrize("dims,ranks", [((20, 20, 20, 5), [1, 7, 30, 5, 1]), ((20, 20, 20, 5, 4), [1, 9, 60, 11, 3, 1]),
+                                        ((5, 20, 20, 20), [1, 5, 70, 20, 1])])
+def test_example2_sizes_low_rank(dims, ranks):
+    """Trains of known ranks at Example 2's sizes: eps = 1e-5 recovers the construction's ranks and O6's cores."""
+    rng = np.random.default_rng(sum(ranks))
+    Xs = [ref.dense_from_tt(ref.random_train(rng, dims, ranks)) for _ in range(3)]
+    Xs = [x.astype(np.float32).astype(np.float64) for x in Xs]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 1e-5)
+    for b, cs in enumerate(_trains(T)):
+        want = ttsvd.tt_svd(Xs[b], 1e-5)
+        assert [c.shape[0] for c in cs] + [1] == ranks
+        assert [c.shape for c in cs] == [w.shape for w in want]
+        for c, w in zip(cs, want):
+            assert np.max(np.abs(c - w)) <= 1e-4 * np.max(np.abs(w)), "core mismatch"
+
+
+@pytest.mark.parametrize("eps", [0.1, 0.3])
+def test_example2_error_guarantee(eps):
+    """||X - TT(X)|| <= eps ||X|| (Alg. 1's guarantee) on case (iii), ranks within one of O6's."""
+    dims = EXAMPLE2[1]
+    rng = np.random.default_rng(int(100 * eps))
+    Xs = [rng.standard_normal(dims).astype(np.float32).astype(np.float64) for _ in range(2)]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, eps)
+    for b, cs in enumerate(_trains(T)):
+        err = np.linalg.norm(ref.dense_from_tt(cs) - Xs[b])
+        assert err <= eps * np.linalg.norm(Xs[b]) * (1 + 1e-4)
+        want = ttsvd.tt_svd(Xs[b], eps)
+        assert all(abs(c.shape[2] - w.shape[2]) <= 1 for c, w in zip(cs[:-1], want[:-1]))
+
+
+def test_example2_case_ii_alg2_on_gpu():
+    """Example 2 case (ii) end to end on the GPU: X x_1^1 Y of two 20 x 20 x 20 x 5 Gaussian tensors through
+    TT-SVD (workspace kernel), splice, reconstruction == Eq. 8 (eps = 0: exact up to rounding)."""
+    dims = EXAMPLE2[0]
+    rng = np.random.default_rng(11)
+    B = 2
+    Xs = [rng.standard_normal(dims).astype(np.float32).astype(np.float64) for _ in range(B)]
+    Ys = [rng.standard_normal(dims).astype(np.float32).astype(np.float64) for _ in range(B)]
+    TX = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 0.0)
+    TY = ttc.ttc_tt_svd(_dense_batch(Ys), dims, 0.0)
+    plan = ttc.ttc_splice_plan_create(TX, TY, 1, 1)
+    cores, ranks, offs = ttc.ttc_contract(plan, TX, TY)
+    Z = ttc.TTDevice(cores, plan.dims, ranks=ranks, offsets=offs)
+    dense = ttc.ttc_reconstruct(Z, plan.perm).cpu().numpy().astype(np.float64)
+    n_el = (20 * 20 * 5) ** 2
+    for b in range(B):
+        want = ref.tcp(Xs[b], Ys[b], [1], [1])
+        got = dense[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
+        err = np.linalg.norm(got - want) / (np.linalg.norm(Xs[b]) * np.linalg.norm(Ys[b]))
+        assert err <= 1e-5, f"pair {b}: {err:.3e}"
