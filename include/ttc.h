@@ -45,6 +45,8 @@ extern "C" {
 #define TTC_MAX_ORDER 256   /* ttc_inner: N <= 256 */
 #define TTC_MAX_CONTRACT_ORDER 64  /* ttc_contract: N, M <= 64 */
 #define TTC_MAX_RANK 128    /* every bond rank <= 128 (larger: TTC_ERR_UNSUPPORTED) */
+#define TTC_MAX_SPLICE_RANK 1024   /* ttc_splice_plan_create / its ttc_contract / ttc_reconstruct: ranks <= 1024
+                                      (the TT-SVD of Example 2's order-5 tensor has R_2 = 400) */
 
 typedef enum {
     TTC_OK = 0,

@@ -31,7 +31,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 TTC_OK, TTC_ERR_NULL, TTC_ERR_SHAPE, TTC_ERR_RANK, TTC_ERR_MODES = 0, 1, 2, 3, 4
 TTC_ERR_ALIGN, TTC_ERR_OVERFLOW, TTC_ERR_UNSUPPORTED, TTC_ERR_CUDA, TTC_ERR_ARG = 5, 6, 7, 8, 9
-TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK = 256, 64, 128
+TTC_MAX_ORDER, TTC_MAX_CONTRACT_ORDER, TTC_MAX_RANK, TTC_MAX_SPLICE_RANK = 256, 64, 128, 1024
 
 EXPORTED = ("ttc_inner", "ttc_inner_ordered", "ttc_contract_plan_create", "ttc_splice_plan_create", "ttc_contract_plan_query",
             "ttc_contract_plan_layout", "ttc_reconstruct", "ttc_reconstruct_workspace", "ttc_reconstruct_ws",

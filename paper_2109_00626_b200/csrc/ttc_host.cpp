@@ -47,7 +47,8 @@ struct HostTrain {
 };
 
 // A1: validate one operand batch; `name` is "X" or "Y".
-ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, HostTrain* h) {
+ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, HostTrain* h,
+                       int max_rank = TTC_MAX_RANK) {
     if (!t) return fail(TTC_ERR_NULL, "%s: batch descriptor is NULL", name);
     if (t->batch < 0) return fail(TTC_ERR_ARG, "%s: batch = %d < 0", name, t->batch);
     if (t->order < 1) return fail(TTC_ERR_SHAPE, "%s: order N = %d < 1", name, t->order);
@@ -65,8 +66,8 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
             return fail(TTC_ERR_ARG, "%s: ranks_dev given without ranks_host", name);
         if (t->order > 1) {
             if (t->uniform_rank < 1) return fail(TTC_ERR_RANK, "%s: uniform_rank = %d < 1", name, t->uniform_rank);
-            if (t->uniform_rank > TTC_MAX_RANK)
-                return fail(TTC_ERR_UNSUPPORTED, "%s: uniform_rank = %d > %d", name, t->uniform_rank, TTC_MAX_RANK);
+            if (t->uniform_rank > max_rank)
+                return fail(TTC_ERR_UNSUPPORTED, "%s: uniform_rank = %d > %d", name, t->uniform_rank, max_rank);
             h->urank = t->uniform_rank;
             h->mult8 = (h->urank & 7) == 0;
         }
@@ -87,7 +88,7 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
             int64_t elems = (int64_t)t->dims[0] * r[1];
             for (int n = 1; n < N; ++n) {
                 const int v = r[n];
-                bad |= (v < 1) | (v > TTC_MAX_RANK);
+                bad |= (v < 1) | (v > max_rank);
                 mr = v > mr ? v : mr;
                 or8 |= (unsigned)v;
                 elems += (int64_t)v * t->dims[n] * r[n + 1];
@@ -102,8 +103,8 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
                                 r[0], r[N]);
                 for (int n = 1; n < N; ++n) {
                     if (r[n] < 1) return fail(TTC_ERR_RANK, "%s pair %d: rank R_%d = %d < 1", name, b, n, r[n]);
-                    if (r[n] > TTC_MAX_RANK)
-                        return fail(TTC_ERR_UNSUPPORTED, "%s pair %d: rank R_%d = %d > %d", name, b, n, r[n], TTC_MAX_RANK);
+                    if (r[n] > max_rank)
+                        return fail(TTC_ERR_UNSUPPORTED, "%s pair %d: rank R_%d = %d > %d", name, b, n, r[n], max_rank);
                 }
             }
         }
@@ -122,7 +123,7 @@ ttc_status check_batch(const ttc_tt_batch* t, const char* name, int max_order, H
     if (t->cores && (reinterpret_cast<uintptr_t>(t->cores) & 3u))
         return fail(TTC_ERR_ALIGN, "%s: cores pointer not 4-byte aligned", name);
     // sizes and bounds, overflow-checked.  A train has at most TTC_MAX_ORDER cores of at most
-    // TTC_MAX_RANK^2 * (2^31 - 1) elements, < 2^53: its size cannot overflow; offset + size can.
+    // TTC_MAX_SPLICE_RANK^2 * (2^31 - 1) elements, < 2^52: its size cannot overflow; offset + size can.
     const int N = t->order;
     if (h->uniform) {
         int64_t elems = 0;
@@ -364,7 +365,7 @@ ttc_status reconstruct_impl(const ttc_tt_batch* t, const int32_t* perm, float* o
     if (query) *query = 0;
     HostTrain h;
     ttc_status st;
-    if ((st = check_batch(t, "T", TTC_MAX_ORDER, &h)) != TTC_OK) return st;
+    if ((st = check_batch(t, "T", TTC_MAX_ORDER, &h, TTC_MAX_SPLICE_RANK)) != TTC_OK) return st;
     const int N = t->order, B = t->batch;
     // output strides of the train's modes: output mode c is train mode perm[c] (1-based)
     std::vector<int64_t> ostride(N, 0);
@@ -900,8 +901,8 @@ ttc_status ttc_splice_plan_create(const ttc_tt_batch* x, const ttc_tt_batch* y, 
     *plan = nullptr;
     HostTrain hx, hy;
     ttc_status st;
-    if ((st = check_batch(x, "X", ttc::kMaxContractOrder, &hx)) != TTC_OK) return st;
-    if ((st = check_batch(y, "Y", ttc::kMaxContractOrder, &hy)) != TTC_OK) return st;
+    if ((st = check_batch(x, "X", ttc::kMaxContractOrder, &hx, TTC_MAX_SPLICE_RANK)) != TTC_OK) return st;
+    if ((st = check_batch(y, "Y", ttc::kMaxContractOrder, &hy, TTC_MAX_SPLICE_RANK)) != TTC_OK) return st;
     if (x->batch != y->batch) return fail(TTC_ERR_SHAPE, "batch mismatch: X has %d trains, Y has %d", x->batch, y->batch);
     const int N = x->order, M = y->order;
     if (x_mode != 1 && x_mode != N)
@@ -1020,8 +1021,8 @@ ttc_status ttc_contract(const ttc_contract_plan* p, const ttc_tt_batch* x, const
     if (!p) return fail(TTC_ERR_NULL, "plan is NULL");
     HostTrain hx, hy;
     ttc_status st;
-    if ((st = check_batch(x, "X", ttc::kMaxContractOrder, &hx)) != TTC_OK) return st;
-    if ((st = check_batch(y, "Y", ttc::kMaxContractOrder, &hy)) != TTC_OK) return st;
+    if ((st = check_batch(x, "X", ttc::kMaxContractOrder, &hx, p->splice ? TTC_MAX_SPLICE_RANK : TTC_MAX_RANK)) != TTC_OK) return st;
+    if ((st = check_batch(y, "Y", ttc::kMaxContractOrder, &hy, p->splice ? TTC_MAX_SPLICE_RANK : TTC_MAX_RANK)) != TTC_OK) return st;
     if (x->batch != p->B || y->batch != p->B || x->order != p->N || y->order != p->M)
         return fail(TTC_ERR_SHAPE, "operands (B=%d/%d, N=%d, M=%d) differ from the plan (B=%d, N=%d, M=%d)", x->batch,
                     y->batch, x->order, y->order, p->B, p->N, p->M);

@@ -217,12 +217,14 @@ def test_example2_error_guarantee(eps):
         assert all(abs(c.shape[2] - w.shape[2]) <= 1 for c, w in zip(cs[:-1], want[:-1]))
 
 
-def test_example2_case_ii_alg2_on_gpu():
-    """Example 2 case (ii) end to end on the GPU: X x_1^1 Y of two 20 x 20 x 20 x 5 Gaussian tensors through
-    TT-SVD (workspace kernel), splice, reconstruction == Eq. 8 (eps = 0: exact up to rounding)."""
-    dims = EXAMPLE2[0]
-    rng = np.random.default_rng(11)
-    B = 2
+@pytest.mark.parametrize("case", [0, 1])
+def test_example2_alg2_on_gpu(case):
+    """Example 2 cases (ii) and (iii) end to end on the GPU: X x_1^1 Y of two 20 x 20 x 20 x 5 (x 4) Gaussian
+    tensors through TT-SVD (workspace kernel), splice (ranks up to 400 in case (iii)), reconstruction (workspace
+    GEMM chain; 4,000,000 / 64,000,000 entries per pair) == Eq. 8 (eps = 0: exact up to rounding)."""
+    dims = EXAMPLE2[case]
+    rng = np.random.default_rng(11 + case)
+    B = 2 - case
     Xs = [rng.standard_normal(dims).astype(np.float32).astype(np.float64) for _ in range(B)]
     Ys = [rng.standard_normal(dims).astype(np.float32).astype(np.float64) for _ in range(B)]
     TX = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 0.0)
@@ -231,7 +233,7 @@ def test_example2_case_ii_alg2_on_gpu():
     cores, ranks, offs = ttc.ttc_contract(plan, TX, TY)
     Z = ttc.TTDevice(cores, plan.dims, ranks=ranks, offsets=offs)
     dense = ttc.ttc_reconstruct(Z, plan.perm).cpu().numpy().astype(np.float64)
-    n_el = (20 * 20 * 5) ** 2
+    n_el = int(np.prod(dims[1:])) ** 2
     for b in range(B):
         want = ref.tcp(Xs[b], Ys[b], [1], [1])
         got = dense[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
