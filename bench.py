@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-sub", action="store_true", help="main line only (no C1/C3/C4/C5 sub-results)")
+    p.add_argument("--example2", action="store_true", help="Example 2 / Fig. 4a: TTCP vs Eq. 8, cases (i)-(iii)")
     p.add_argument("--sub", default=",".join(SUB_CONFIGS), help="comma list of sub-result configs")
     return p.parse_args()
 
@@ -171,8 +172,8 @@ def _oracle_pairs(cfg, X, Y, count, nthreads):
                                      count)
     elif c["op"] == "alg2":          # O6: the dense-input TTCP pipeline per pair (numpy)
         from oracle import ttsvd
-        n_el = c["I"] ** c["N"]
-        shape = (c["I"],) * c["N"]
+        shape = ttgen.alg2_shape(cfg)
+        n_el = int(np.prod(shape))
         xh, yh = X.cpu().numpy(), Y.cpu().numpy()
         for b in range(count):
             ttsvd.ttcp_dense(xh[b * n_el:(b + 1) * n_el].reshape(shape, order="F"),
@@ -200,7 +201,7 @@ def cpu_oracle_rate(cfg: str, X, Y, target_s: float, nthreads: int = None, one_t
         _oracle_pairs(cfg, X, Y, count, nt)
         return time.perf_counter() - t0
 
-    nb = X.B if hasattr(X, "B") else X.numel() // (ttgen.CONFIGS[cfg]["I"] ** ttgen.CONFIGS[cfg]["N"])
+    nb = X.B if hasattr(X, "B") else X.numel() // int(np.prod(ttgen.alg2_shape(cfg)))
     probe = max(1, min(nb, nthreads))
     t = run(probe, nthreads)
     count = int(min(nb, max(probe, probe * target_s / max(t, 1e-6))))
@@ -290,9 +291,10 @@ def make_work(ttc, cfg, b0, B, seed, dev, stream, ranks=None):
     elif c["op"] == "alg2":
         # Alg. 2 on dense operands: TT-SVD of X^rho and Y^rho (step 1's permutation folded into the read),
         # K and the splice (steps 4-5), dense reconstruction in Eq. 8 order (steps 5-6)
-        shape = (c["I"],) * c["N"]
-        px = [c["x_mode"]] + [k for k in range(1, c["N"] + 1) if k != c["x_mode"]]
-        py = [c["y_mode"]] + [k for k in range(1, c["N"] + 1) if k != c["y_mode"]]
+        shape = ttgen.alg2_shape(cfg)
+        Nd = len(shape)
+        px = [c["x_mode"]] + [k for k in range(1, Nd + 1) if k != c["x_mode"]]
+        py = [c["y_mode"]] + [k for k in range(1, Nd + 1) if k != c["y_mode"]]
         TX = ttc.ttc_tt_svd(X, shape, c["eps"], perm=px)
         TY = ttc.ttc_tt_svd(Y, shape, c["eps"], perm=py)
         plan = ttc.ttc_splice_plan_create(TX, TY, 1, 1)
@@ -305,25 +307,41 @@ def make_work(ttc, cfg, b0, B, seed, dev, stream, ranks=None):
         rk_x, rk_y = torch.empty_like(rx_dev), torch.empty_like(ry_dev)
         ws_x = torch.empty(max(16, ttc.ttc_tt_svd_workspace(B, shape, px)), dtype=torch.uint8, device=dev)
         ws_y = torch.empty(max(16, ttc.ttc_tt_svd_workspace(B, shape, py)), dtype=torch.uint8, device=dev)
-        n_in = c["I"] ** c["N"]
+        nb_r = ttc.ttc_reconstruct_workspace(ZD, plan.perm)
+        ws_r = torch.empty(nb_r, dtype=torch.uint8, device=dev) if nb_r else None
+        n_in = int(np.prod(shape))
         train_x = int(sum(int(a) * int(i) * int(b2) for a, i, b2 in
                           zip(TX.rank_rows()[0][:-1], TX.dims_np, TX.rank_rows()[0][1:])))
         w.alg_bytes = 4.0 * B * (2 * n_in + 2 * 2 * train_x + 2 * (plan.total // B) + n_out)
-        R1, I = int(TX.rank_rows()[0][1]), c["I"]
-        svd_mac = 2 * (I * I * n_in // I + 2 * I ** 3 * R1 + 12 * (I - 1) * (I // 2) * I * 6)
-        w.alg_flops = 2.0 * B * (svd_mac + I * R1 * R1 + R1 * R1 * I * R1 + n_out * R1 + 2 * I * I * R1 * R1)
+        if cfg == "A2":   # cube 20^3: Gram + Jacobi + products of the two SVD steps, K, splice, reconstruction
+            R1, I = int(TX.rank_rows()[0][1]), c["I"]
+            svd_mac = 2 * (I * I * n_in // I + 2 * I ** 3 * R1 + 12 * (I - 1) * (I // 2) * I * 6)
+            w.alg_flops = 2.0 * B * (svd_mac + I * R1 * R1 + R1 * R1 * I * R1 + n_out * R1 + 2 * I * I * R1 * R1)
+        else:             # iterative (one-sided Jacobi) TT-SVD: no fixed flop count; the HBM roofline only
+            w.alg_flops = 0.0
 
-        def step():
+        def svd():
             ttc.ttc_tt_svd_into(X, shape, c["eps"], TX.cores, rk_x, perm=px, stream=stream, workspace=ws_x)
             ttc.ttc_tt_svd_into(Y, shape, c["eps"], TY.cores, rk_y, perm=py, stream=stream, workspace=ws_y)
+
+        def splice():
             ttc.ttc_contract(plan, TX, TY, out=zc, stream=stream)
-            ttc.ttc_reconstruct(ZD, plan.perm, out=out, stream=stream)
+
+        def recon():
+            ttc.ttc_reconstruct(ZD, plan.perm, out=out, stream=stream, workspace=ws_r)
+
+        def step():
+            svd()
+            splice()
+            recon()
+        w.stages = {"tt_svd_x_and_y": svd, "splice": splice, "reconstruct": recon}
         w.kernel = "alg2 pipeline (ttsvd x2, splice, reconstruct)"
-        # ttc_tt_svd is 1 + 2 (N - 1) launches when every Gram side is <= 32 (the warp-Jacobi pipeline) else 1
-        dims_full = [c["I"]] * c["N"]
-        side = max(min(int(np.prod(dims_full[:n + 1])), int(np.prod(dims_full[n + 1:]))) for n in range(c["N"] - 1))
-        per_svd = 1 + 2 * (c["N"] - 1) if side <= 32 else 1
-        w.launches = 2 * per_svd + 2
+        # ttc_tt_svd is 1 + 2 (N - 1) launches when every Gram side is <= 32 (the warp-Jacobi pipeline) else 1;
+        # the reconstruction 1 launch (shared memory) or L - 1 (workspace GEMM chain, L = output order)
+        side = max(min(int(np.prod(shape[:n + 1])), int(np.prod(shape[n + 1:]))) for n in range(Nd - 1))
+        per_svd = 1 + 2 * (Nd - 1) if side <= 32 else 1
+        w.launches = 2 * per_svd + 1 + (len(plan.dims) - 1 if nb_r else 1)
+        w.plan, w.TX = plan, TX
     elif c["op"] == "reconstruct":
         n_el = c["I"] ** c["N"]
         out = torch.empty(B * n_el, dtype=torch.float32, device=dev)
@@ -520,6 +538,78 @@ def run_sub(ttc, cfg, args, rank, world, dev, stream, peaks, peak_kind, flush_bu
     return res
 
 
+def run_example2(ttc, args, dev, stream, peaks, peak_kind, flush_buf):
+    """Example 2 (Fig. 4a): X x_1^1 Y of two zero-mean unit-variance Gaussian tensors, cases
+    (i) 20^3, (ii) 20 x 20 x 20 x 5, (iii) 20 x 20 x 20 x 5 x 4, "both in the original form via Eq. 8 and through
+    the proposed TTCP algorithm" (time including the TT decompositions).  On the GPU: the TTCP pipeline (TT-SVD
+    of both operands, K + splice, and the dense reconstruction in Eq. 8 order) and, as the dense-TCP baseline,
+    Eq. 8 as one batched fp32 GEMM (cuBLAS through torch.bmm: Z^T = Y_(1)^T X_(1), a plain library GEMM).  On
+    the host: the oracle's TTCP (O6, numpy) and Eq. 8 by numpy tensordot on a bounded sample.  The paper prints
+    no times for this figure, so there is nothing to compare against but the two arms."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    cases = []
+    clocks = ClockSampler(dev.index or 0).start()
+    for cfg, label in (("A2", "i"), ("A2ii", "ii"), ("A2iii", "iii")):
+        c = ttgen.CONFIGS[cfg]
+        B = c["B"]
+        shape = ttgen.alg2_shape(cfg)
+        w = make_work(ttc, cfg, 0, B, args.seed, dev, stream)
+        fb = flush_buf if w.working_set < 2 * L2_BYTES else None
+        steps, warm = 3, 3
+        ms = statistics.median(time_region(w.step, stream, dev, steps, warm, fb, 1))
+        stages = {k: statistics.median(time_region(f, stream, dev, steps, warm, fb, 1)) / B
+                  for k, f in w.stages.items()}
+        # dense-TCP baseline: Eq. 8 as one batched GEMM on the same operands (unfoldings read in place)
+        I1 = shape[0]
+        rest = int(np.prod(shape[1:]))
+        Xt, Yt = w.X.view(B, rest, I1), w.Y.view(B, rest, I1)
+        dense = torch.empty((B, rest, rest), dtype=torch.float32, device=dev)
+
+        def eq8():
+            torch.bmm(Yt, Xt.transpose(1, 2), out=dense)
+        ms_eq8 = statistics.median(time_region(eq8, stream, dev, steps, warm, fb, 1))
+        # sanity: the two arms agree on pair 0 (eps = 0: exact TTCP up to rounding)
+        n_out = rest * rest
+        a0 = w.out[:n_out].view(rest, rest)
+        rel = float((a0 - dense[0]).norm() / dense[0].norm())
+        case = {"case": label, "workload": cfg, "shape": list(shape), "pairs": B, "eps": c["eps"],
+                "ttcp_ms_per_pair": ms / B, "ttcp_stage_ms_per_pair": stages,
+                "ttcp_tt_result_ms_per_pair": stages["tt_svd_x_and_y"] + stages["splice"],
+                "eq8_gemm_ms_per_pair": ms_eq8 / B, "eq8_over_ttcp": (ms_eq8 / B) / (ms / B),
+                "tt_ranks_x": [int(v) for v in w.TX.rank_rows()[0]], "output_entries": n_out,
+                "rel_diff_pair0": rel, "gpu_launches_per_step": w.launches,
+                "roofline": roofline_for(w, ms, peaks, peak_kind, cfg, B),
+                "l2": "flushed between steps (2x L2 write)" if fb is not None else "inputs larger than L2"}
+        if not args.no_cpu:
+            from oracle import ttsvd
+            xh, yh = w.X[:rest * I1].cpu().numpy(), w.Y[:rest * I1].cpu().numpy()
+            x0 = xh.astype(np.float64).reshape(shape, order="F")
+            y0 = yh.astype(np.float64).reshape(shape, order="F")
+            reps = 0
+            t0 = time.perf_counter()
+            while reps == 0 or (time.perf_counter() - t0 < 3.0 and reps < 50):
+                ttsvd.ttcp_dense(x0, y0, 1, 1, c["eps"])
+                reps += 1
+            t_ttcp = (time.perf_counter() - t0) / reps
+            reps2 = 0
+            t0 = time.perf_counter()
+            while reps2 == 0 or (time.perf_counter() - t0 < 3.0 and reps2 < 50):
+                np.tensordot(x0, y0, axes=([0], [0]))
+                reps2 += 1
+            t_eq8 = (time.perf_counter() - t0) / reps2
+            case["cpu"] = {"ttcp_oracle_ms_per_pair": 1e3 * t_ttcp, "eq8_tensordot_ms_per_pair": 1e3 * t_eq8,
+                           "cores": len(os.sched_getaffinity(0)), "kind": "oracle", "cpu_model": cpu_model(),
+                           "sample": f"pair 0: O6 ttcp_dense x{reps}, numpy tensordot x{reps2} (fp64)"}
+        cases.append(case)
+        del w, dense, Xt, Yt
+        torch.cuda.empty_cache()
+    clk = clocks.stop()
+    line = {"mode": "example2", "metric": "Example 2 (Fig. 4a): ms per pair, TTCP incl. TT-SVD vs Eq. 8",
+            "unit": "ms/pair", "higher_is_better": False, "n_gpus": 1, "dtype": "f32 (TT-SVD in f64)",
+            "data": "synthetic N(0,1) dense tensors, seeded", "cases": cases, "clocks": clk}
+    print(json.dumps(line))
+
+
 def spawn(args):
     """--gpus N without a torch.distributed environment: re-launch this script with N ranks (one per GPU)."""
     import socket
@@ -562,6 +652,10 @@ def main():
     stream = torch.cuda.current_stream(dev)
     peaks, peak_kind = load_peaks()
     flush_buf = torch.empty(int(2 * L2_BYTES // 4), dtype=torch.float32, device=dev)
+    if args.example2:
+        if rank == 0:
+            run_example2(ttc, args, dev, stream, peaks, peak_kind, flush_buf)
+        return
 
     # ---- main line: weak scaling, this rank's B pairs (pairs rank*B .. rank*B + B - 1 of the global batch)
     w = make_work(ttc, cfg, rank * B, B, args.seed, dev, stream)

@@ -41,9 +41,19 @@ CONFIGS = {
     "R1": dict(op="reconstruct", B=1024, N=4, I=20, R=20),
     # the whole dense-input TTCP of Alg. 2 on Example 2 case (i): pairs of
     # zero-mean unit-variance Gaussian 20 x 20 x 20 tensors, x_1^1, TT-SVD at eps = 0 (full ranks 20)
-    "A2": dict(op="alg2", B=1024, N=3, I=20, x_mode=1, y_mode=1, eps=0.0),
+    "A2": dict(op="alg2", B=1024, N=3, I=20, shape=(20, 20, 20), x_mode=1, y_mode=1, eps=0.0),
+    # Example 2 cases (ii) and (iii): 20 x 20 x 20 x 5 and 20 x 20 x 20 x 5 x 4 (full TT ranks [1, 20, 100, 5, 1]
+    # and [1, 20, 400, 20, 4, 1]; TTCP outputs of 4,000,000 and 64,000,000 entries per pair)
+    "A2ii": dict(op="alg2", B=64, N=4, I=20, shape=(20, 20, 20, 5), x_mode=1, y_mode=1, eps=0.0),
+    "A2iii": dict(op="alg2", B=8, N=5, I=20, shape=(20, 20, 20, 5, 4), x_mode=1, y_mode=1, eps=0.0),
 }
-CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "S1": 6, "R1": 7, "A2": 8}
+CFG_ID = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "S1": 6, "R1": 7, "A2": 8, "A2ii": 9, "A2iii": 10}
+
+
+def alg2_shape(cfg: str):
+    """Dense operand shape of an "alg2" workload."""
+    c = CONFIGS[cfg]
+    return tuple(c.get("shape", (c["I"],) * c["N"]))
 
 DEFAULT_SEED = 20210901  # arXiv 2109.00626 submission month; recorded in every bench line
 SIDE_X, SIDE_Y = 0, 1
@@ -258,7 +268,7 @@ def dense_pairs(cfg: str, b0: int = 0, B: Optional[int] = None, seed: int = DEFA
     (Example 2: zero-mean, unit-variance Gaussian tensors)."""
     c = CONFIGS[cfg]
     B = c["B"] if B is None else B
-    n_el = c["I"] ** c["N"]
+    n_el = int(np.prod(alg2_shape(cfg)))
     out = []
     for side in (SIDE_X, SIDE_Y):
         host = torch.empty(B * n_el, dtype=torch.float32)
