@@ -29,11 +29,14 @@ constexpr int kPart = 2 * 32 * 4;   // floats of one warp's partial Z' (2 n-tile
 #define TTC_R16_STAGES 3
 #endif
 constexpr int kStages = TTC_R16_STAGES;   // TMA ring depth (interior steps in flight per CTA)
+constexpr int kScrLd = 17;                // row stride of the boundary warp's scratch cores (16 + 1)
+constexpr int kScr = 2 * 16 * kScrLd;     // floats of the scratch
 
 struct R16Layout {
     int ps_max;      // plane stride for the largest I
     int x_floats;    // X region of a stage (16 planes)
     int stage_floats;
+    int scratch;     // 1: the boundary warp stages its cores in shared memory (I_1, I_N <= 16)
 };
 
 // The k-th pair of this CTA (pairs blockIdx.x, blockIdx.x + gridDim.x, ...): index b and core offsets.
@@ -152,6 +155,7 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
     float* zfrag = zpart + kCW * kPart;           // [slot]: B fragments of Z for the next step
     float* z1buf = zfrag + kCT;                   // [slot]: Z_1 of the next pair (boundary warp)
     float* dbuf = z1buf + kCT;                    // [slot]: sum_i X_N[zg,i,0] Y_N[zf,i,0] of the next pair
+    float* scr = lay.scratch ? dbuf + kCT : nullptr;   // boundary warp: two 16 x kScrLd cores (I_1, I_N <= 16)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int N = a.N, I0 = a.dims[0], IL = a.dims[N - 1];
 
@@ -198,6 +202,51 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
             if (!p.valid) break;
             const float* xs = a.x.cores + p.xo;
             const float* ys = a.y.cores + p.yo;
+            if (scr) {
+                // both cores of a boundary step into the scratch as rows of 16 (+1 pad: conflict-free reads) --
+                // all loads of a core pair in flight at once -- then the 256 dot products from shared memory
+                //   Z_1: row s of X_1 = X_1[0, :, s] (contiguous), row q of Y_1 likewise
+                for (int e = lane; e < 16 * I0; e += 32) {
+                    const int s_ = e / I0, i = e - s_ * I0;
+                    scr[s_ * kScrLd + i] = __ldg(xs + e);
+                    scr[16 * kScrLd + s_ * kScrLd + i] = __ldg(ys + e);
+                }
+                __syncwarp();
+                if (k > 0) mbar_wait(&z1empty, (k - 1) & 1);
+                for (int e = lane; e < kCT; e += 32) {
+                    int zg, zf;
+                    slot_entry(e, zg, zf);
+                    const float* xr = scr + zg * kScrLd;
+                    const float* yr = scr + 16 * kScrLd + zf * kScrLd;
+                    float d = 0.f;
+                    for (int i = 0; i < I0; ++i) d = fmaf(xr[i], yr[i], d);
+                    z1buf[e] = d;
+                }
+                mbar_arrive(&z1full);
+                __syncwarp();
+                //   D: row r of X_N = X_N[r, :, 0] (stride 16 in memory), row p of Y_N likewise
+                const float* xl = xs + last;
+                const float* yl = ys + last;
+                for (int e = lane; e < 16 * IL; e += 32) {
+                    const int r = e & 15, i = e >> 4;
+                    scr[r * kScrLd + i] = __ldg(xl + e);
+                    scr[16 * kScrLd + r * kScrLd + i] = __ldg(yl + e);
+                }
+                __syncwarp();
+                if (k > 0) mbar_wait(&dempty, (k - 1) & 1);
+                for (int e = lane; e < kCT; e += 32) {
+                    int zg, zf;
+                    slot_entry(e, zg, zf);
+                    const float* xr = scr + zg * kScrLd;
+                    const float* yr = scr + 16 * kScrLd + zf * kScrLd;
+                    float d = 0.f;
+                    for (int i = 0; i < IL; ++i) d = fmaf(xr[i], yr[i], d);
+                    dbuf[e] = d;
+                }
+                __syncwarp();
+                mbar_arrive(&dfull);
+                continue;
+            }
             if (k > 0) mbar_wait(&z1empty, (k - 1) & 1);
             for (int e = lane; e < kCT; e += 32) {
                 int zg, zf;
@@ -324,7 +373,7 @@ bool inner_r16_supported(const InnerArgs& a, bool uniform_r16) {
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
     // two stages of 2 x 16 padded planes + partials + fragments
     const size_t smem = sizeof(float) * (kStages * (size_t)16 * (ps_x(16 * max_dim) + ps_y(16 * max_dim)) + kCW * kPart + 3 * kCT);
-    return smem <= 112 * 1024;   // two CTAs per SM
+    return smem <= 112 * 1024;   // two CTAs per SM (the boundary scratch is added only where it still fits)
 }
 
 cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s) {
@@ -334,7 +383,10 @@ cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s) {
     lay.ps_max = ps_x(16 * max_dim);
     lay.x_floats = 16 * lay.ps_max;
     lay.stage_floats = lay.x_floats + 16 * ps_y(16 * max_dim);
-    const size_t smem = sizeof(float) * (kStages * (size_t)lay.stage_floats + kCW * kPart + 3 * kCT);
+    size_t smem = sizeof(float) * (kStages * (size_t)lay.stage_floats + kCW * kPart + 3 * kCT);
+    // two CTAs per SM: 228 KB less 1 KB reserved and ~0.2 KB static shared memory per CTA
+    lay.scratch = (a.dims[0] <= 16 && a.dims[a.N - 1] <= 16 && smem + sizeof(float) * kScr <= 113 * 1024) ? 1 : 0;
+    if (lay.scratch) smem += sizeof(float) * kScr;
     cudaError_t e = cudaFuncSetAttribute(inner_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
