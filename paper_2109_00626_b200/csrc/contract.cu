@@ -229,6 +229,85 @@ __device__ __forceinline__ void emit_fast(const FreeCore& f, const float* TL, in
     }
 }
 
+// The same emission when nb divides Bs (every thread's betas share its rr residue): nested loops with the
+// absorbed transfer's columns held in registers across the inner loop -- KIND 1 (TL (X (x) I)): TL[a0.., r + R pp]
+// depends on pp only, so pp is the outer loop; KIND 3 (TL (I (x) Y)): TL[a0.., rr + H q] depends on rr only, so
+// rr is the outer loop.  R = 4 RQ (RQ <= 2: the cached quads stay within the 64-register budget).
+template <int KIND, int RQ>
+__device__ __forceinline__ void emit_nested(const FreeCore& f, const float* TL, int Aout, int Bout, int Q, int Bs,
+                                            float* dst) {
+    constexpr int R = 4 * RQ;
+    const int I = f.I;
+    const int qpa = Aout >> 2, nb = blockDim.x / Q;
+    const int t = threadIdx.x;
+    if (t >= nb * Q) return;
+    const int a0 = 4 * (t % qpa), i = (t / qpa) % I, g0 = t / Q;
+    const int blk = KIND < 2 ? R : f.H;
+    const int pblk = a0 / blk, roff = a0 - blk * pblk;
+    const int np = Bout / Bs;
+    const int64_t cstride = (int64_t)Aout * I;   // floats between consecutive output columns beta
+    float* d0 = dst + a0 + (int64_t)Aout * i;
+    const float* gbase = f.G + R * i;
+    const int gstride = R * I;
+    if (KIND == 1) {
+        for (int pp = 0; pp < np; ++pp) {
+            float4 tq[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) tq[r] = *reinterpret_cast<const float4*>(TL + a0 + Aout * (r + R * pp));
+            for (int rr = g0; rr < Bs; rr += nb) {
+                const float* gcol = gbase + gstride * rr;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f), v2 = v;
+#pragma unroll
+                for (int r = 0; r < R; r += 4) {
+                    const float4 g = *reinterpret_cast<const float4*>(gcol + r);
+                    quad_fma(v, tq[r], g.x);
+                    quad_fma(v2, tq[r + 1], g.y);
+                    quad_fma(v, tq[r + 2], g.z);
+                    quad_fma(v2, tq[r + 3], g.w);
+                }
+                st_cs4(d0 + cstride * (rr + Bs * pp), v.x + v2.x, v.y + v2.y, v.z + v2.z, v.w + v2.w);
+            }
+        }
+    } else if (KIND == 3) {
+        const int hs = Aout * f.H;
+        for (int rr = g0; rr < Bs; rr += nb) {
+            float4 tq[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) tq[q] = *reinterpret_cast<const float4*>(TL + a0 + Aout * rr + hs * q);
+            for (int pp = 0; pp < np; ++pp) {
+                const float* gcol = gbase + gstride * pp;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f), v2 = v;
+#pragma unroll
+                for (int q = 0; q < R; q += 4) {
+                    const float4 g = *reinterpret_cast<const float4*>(gcol + q);
+                    quad_fma(v, tq[q], g.x);
+                    quad_fma(v2, tq[q + 1], g.y);
+                    quad_fma(v, tq[q + 2], g.z);
+                    quad_fma(v2, tq[q + 3], g.w);
+                }
+                st_cs4(d0 + cstride * (rr + Bs * pp), v.x + v2.x, v.y + v2.y, v.z + v2.z, v.w + v2.w);
+            }
+        }
+    } else if (KIND == 0) {   // rows r + R pp carry X[r, i, rr]: only pp == pblk is nonzero
+        for (int pp = 0; pp < np; ++pp)
+            for (int rr = g0; rr < Bs; rr += nb) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (pp == pblk) v = *reinterpret_cast<const float4*>(gbase + gstride * rr + roff);
+                st_cs4(d0 + cstride * (rr + Bs * pp), v.x, v.y, v.z, v.w);
+            }
+    } else {                  // rows rr + H p carry Y[p, j, pp]: the quad holds row rr + H pblk iff rr - roff < 4
+        for (int rr = g0; rr < Bs; rr += nb) {
+            const int k = rr - roff;
+            const bool has = (unsigned)k < 4u;   // lanes differ: predicated loads, one store stream per warp
+            for (int pp = 0; pp < np; ++pp) {
+                const float val = has ? gbase[gstride * pp + pblk] : 0.f;
+                st_cs4(d0 + cstride * (rr + Bs * pp), k == 0 ? val : 0.f, k == 1 ? val : 0.f, k == 2 ? val : 0.f,
+                       k == 3 ? val : 0.f);
+            }
+        }
+    }
+}
+
 __device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* xc, const float* yc, int l,
                           const float* TL, const float* TR, float* out) {
     const OutCore& oc = a.outc[l];
@@ -258,6 +337,25 @@ __device__ void emit_core(const ContractArgs& a, const PairCtx& c, const float* 
     // core's column (i, rr) / (i, pp) it reads is contiguous along the summed bond (16-byte loads)
     const bool fast = !has_tr && (Aout & 3) == 0 && (f.Rb & 3) == 0 && aligned && Q <= (int)blockDim.x &&
                       (f.xfree ? true : (f.H & 3) == 0) && total < (1ll << 31);
+    if (fast && Bs % (blockDim.x / Q) == 0 && Bout % Bs == 0 && (f.Rb == 4 || f.Rb == 8)) {
+        const int kind = (f.xfree ? 0 : 2) + (has_tl ? 1 : 0);
+        if (f.Rb == 8) {
+            switch (kind) {
+                case 0: emit_nested<0, 2>(f, TL, Aout, Bout, Q, Bs, dst); break;
+                case 1: emit_nested<1, 2>(f, TL, Aout, Bout, Q, Bs, dst); break;
+                case 2: emit_nested<2, 2>(f, TL, Aout, Bout, Q, Bs, dst); break;
+                default: emit_nested<3, 2>(f, TL, Aout, Bout, Q, Bs, dst); break;
+            }
+        } else {
+            switch (kind) {
+                case 0: emit_nested<0, 1>(f, TL, Aout, Bout, Q, Bs, dst); break;
+                case 1: emit_nested<1, 1>(f, TL, Aout, Bout, Q, Bs, dst); break;
+                case 2: emit_nested<2, 1>(f, TL, Aout, Bout, Q, Bs, dst); break;
+                default: emit_nested<3, 1>(f, TL, Aout, Bout, Q, Bs, dst); break;
+            }
+        }
+        return;
+    }
     if (fast) {
         const int kind = (f.xfree ? 0 : 2) + (has_tl ? 1 : 0);
         switch (kind) {
