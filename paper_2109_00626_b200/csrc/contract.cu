@@ -256,16 +256,16 @@ __device__ __forceinline__ void emit_nested(const FreeCore& f, const float* TL, 
             for (int r = 0; r < R; ++r) tq[r] = *reinterpret_cast<const float4*>(TL + a0 + Aout * (r + R * pp));
             for (int rr = g0; rr < Bs; rr += nb) {
                 const float* gcol = gbase + gstride * rr;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f), v2 = v;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int r = 0; r < R; r += 4) {
                     const float4 g = *reinterpret_cast<const float4*>(gcol + r);
                     quad_fma(v, tq[r], g.x);
-                    quad_fma(v2, tq[r + 1], g.y);
+                    quad_fma(v, tq[r + 1], g.y);
                     quad_fma(v, tq[r + 2], g.z);
-                    quad_fma(v2, tq[r + 3], g.w);
+                    quad_fma(v, tq[r + 3], g.w);
                 }
-                st_cs4(d0 + cstride * (rr + Bs * pp), v.x + v2.x, v.y + v2.y, v.z + v2.z, v.w + v2.w);
+                st_cs4(d0 + cstride * (rr + Bs * pp), v.x, v.y, v.z, v.w);
             }
         }
     } else if (KIND == 3) {
@@ -276,16 +276,16 @@ __device__ __forceinline__ void emit_nested(const FreeCore& f, const float* TL, 
             for (int q = 0; q < R; ++q) tq[q] = *reinterpret_cast<const float4*>(TL + a0 + Aout * rr + hs * q);
             for (int pp = 0; pp < np; ++pp) {
                 const float* gcol = gbase + gstride * pp;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f), v2 = v;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int q = 0; q < R; q += 4) {
                     const float4 g = *reinterpret_cast<const float4*>(gcol + q);
                     quad_fma(v, tq[q], g.x);
-                    quad_fma(v2, tq[q + 1], g.y);
+                    quad_fma(v, tq[q + 1], g.y);
                     quad_fma(v, tq[q + 2], g.z);
-                    quad_fma(v2, tq[q + 3], g.w);
+                    quad_fma(v, tq[q + 3], g.w);
                 }
-                st_cs4(d0 + cstride * (rr + Bs * pp), v.x + v2.x, v.y + v2.y, v.z + v2.z, v.w + v2.w);
+                st_cs4(d0 + cstride * (rr + Bs * pp), v.x, v.y, v.z, v.w);
             }
         }
     } else if (KIND == 0) {   // rows r + R pp carry X[r, i, rr]: only pp == pblk is nonzero
