@@ -249,13 +249,15 @@ __device__ __forceinline__ void emit_nested(const FreeCore& f, const float* TL, 
     float* d0 = dst + a0 + (int64_t)Aout * i;
     const float* gbase = f.G + R * i;
     const int gstride = R * I;
+    const int64_t dcol = cstride * nb, dpp = cstride * Bs;   // output step per thread column / per pp
     if (KIND == 1) {
         for (int pp = 0; pp < np; ++pp) {
             float4 tq[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) tq[r] = *reinterpret_cast<const float4*>(TL + a0 + Aout * (r + R * pp));
-            for (int rr = g0; rr < Bs; rr += nb) {
-                const float* gcol = gbase + gstride * rr;
+            const float* gcol = gbase + gstride * g0;
+            float* dp = d0 + cstride * (g0 + (int64_t)Bs * pp);
+            for (int rr = g0; rr < Bs; rr += nb, gcol += gstride * nb, dp += dcol) {
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int r = 0; r < R; r += 4) {
@@ -265,7 +267,7 @@ __device__ __forceinline__ void emit_nested(const FreeCore& f, const float* TL, 
                     quad_fma(v, tq[r + 2], g.z);
                     quad_fma(v, tq[r + 3], g.w);
                 }
-                st_cs4(d0 + cstride * (rr + Bs * pp), v.x, v.y, v.z, v.w);
+                st_cs4(dp, v.x, v.y, v.z, v.w);
             }
         }
     } else if (KIND == 3) {
@@ -274,8 +276,9 @@ __device__ __forceinline__ void emit_nested(const FreeCore& f, const float* TL, 
             float4 tq[R];
 #pragma unroll
             for (int q = 0; q < R; ++q) tq[q] = *reinterpret_cast<const float4*>(TL + a0 + Aout * rr + hs * q);
-            for (int pp = 0; pp < np; ++pp) {
-                const float* gcol = gbase + gstride * pp;
+            const float* gcol = gbase;
+            float* dp = d0 + cstride * rr;
+            for (int pp = 0; pp < np; ++pp, gcol += gstride, dp += dpp) {
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int q = 0; q < R; q += 4) {
@@ -285,24 +288,29 @@ __device__ __forceinline__ void emit_nested(const FreeCore& f, const float* TL, 
                     quad_fma(v, tq[q + 2], g.z);
                     quad_fma(v, tq[q + 3], g.w);
                 }
-                st_cs4(d0 + cstride * (rr + Bs * pp), v.x, v.y, v.z, v.w);
+                st_cs4(dp, v.x, v.y, v.z, v.w);
             }
         }
     } else if (KIND == 0) {   // rows r + R pp carry X[r, i, rr]: only pp == pblk is nonzero
-        for (int pp = 0; pp < np; ++pp)
-            for (int rr = g0; rr < Bs; rr += nb) {
+        float* dp = d0 + cstride * g0;
+        for (int pp = 0; pp < np; ++pp, dp += dpp) {
+            const float* gp = gbase + gstride * g0 + roff;
+            float* dq = dp;
+            for (int rr = g0; rr < Bs; rr += nb, gp += gstride * nb, dq += dcol) {
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (pp == pblk) v = *reinterpret_cast<const float4*>(gbase + gstride * rr + roff);
-                st_cs4(d0 + cstride * (rr + Bs * pp), v.x, v.y, v.z, v.w);
+                if (pp == pblk) v = *reinterpret_cast<const float4*>(gp);
+                st_cs4(dq, v.x, v.y, v.z, v.w);
             }
+        }
     } else {                  // rows rr + H p carry Y[p, j, pp]: the quad holds row rr + H pblk iff rr - roff < 4
         for (int rr = g0; rr < Bs; rr += nb) {
             const int k = rr - roff;
             const bool has = (unsigned)k < 4u;   // lanes differ: predicated loads, one store stream per warp
-            for (int pp = 0; pp < np; ++pp) {
-                const float val = has ? gbase[gstride * pp + pblk] : 0.f;
-                st_cs4(d0 + cstride * (rr + Bs * pp), k == 0 ? val : 0.f, k == 1 ? val : 0.f, k == 2 ? val : 0.f,
-                       k == 3 ? val : 0.f);
+            const float* gp = gbase + pblk;
+            float* dp = d0 + cstride * rr;
+            for (int pp = 0; pp < np; ++pp, gp += gstride, dp += dpp) {   // selects: exact zeros whatever val is
+                const float val = has ? *gp : 0.f;
+                st_cs4(dp, k == 0 ? val : 0.f, k == 1 ? val : 0.f, k == 2 ? val : 0.f, k == 3 ? val : 0.f);
             }
         }
     }

@@ -1,33 +1,40 @@
 #!/usr/bin/env python
-"""Per-CUDA-source-line instruction counts and stall samples from an ncu report (mixed sass,cuda source view).
-Usage: python tools/ncu_lines.py <report.ncu-rep> [units_for_normalisation] [top]"""
+"""Per-source-line instructions executed and warp-stall samples from an ncu report (CUDA source view; needs
+-lineinfo and --import-source on).  Usage: python tools/ncu_lines.py <report.ncu-rep> [top_n] [kernel_regex]"""
 import csv
 import io
 import subprocess
 import sys
 
-rep = sys.argv[1]
-units = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
-top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(txt)))
-agg = {}
-fn = ""
-for r in rows:
-    if len(r) >= 2 and r[0] == "Function Name":
-        fn = r[1]
-    if len(r) < 8 or r[0] in ("Line No", "File Path", "Function Name") or not r[0]:
-        continue
+
+def num(x):
     try:
-        e, smp = float(r[7]), float(r[4])
+        return int(x)
     except ValueError:
-        continue
-    key = (int(r[0]), r[1].strip()[:80])
-    a = agg.setdefault(key, [0.0, 0.0])
-    a[0] += e
-    a[1] += smp
-tot = sum(v[0] for v in agg.values())
-print(f"total instructions {tot:.4g}  per unit {tot / units:.1f}")
-for (ln, src), (e, s) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{ln:5d} {e / units:9.1f} {100 * e / tot:5.1f}% samples {s:7.0f}  {src}")
+        return 0
+
+
+def main():
+    rep = sys.argv[1]
+    top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if len(sys.argv) > 3:
+        cmd += ["-k", "regex:" + sys.argv[3]]
+    rows = list(csv.reader(io.StringIO(subprocess.run(cmd, capture_output=True, text=True).stdout)))
+    lines, cur = [], None
+    for r in rows:
+        if not r:
+            continue
+        if r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+        elif r[0].isdigit():
+            lines.append((cur, int(r[0]), r[1].strip()[:90], num(r[4]), num(r[7])))
+    ts = sum(x[3] for x in lines) or 1
+    ti = sum(x[4] for x in lines) or 1
+    print(f"samples {ts}, warp instructions {ti}")
+    for f, ln, src, smp, ins in sorted(lines, key=lambda x: -x[3])[:top]:
+        print(f"{f}:{ln:<5} samples {100 * smp / ts:5.1f}%  inst {100 * ins / ti:5.1f}%  {src}")
+
+
+if __name__ == "__main__":
+    main()
