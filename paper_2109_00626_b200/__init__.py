@@ -257,9 +257,12 @@ class ContractPlan:
         self._offsets_dev = None
         self._uniform_out = None
 
+    # bound at class creation: module globals may already be None when a plan is collected at interpreter exit
+    _destroy = _lib.ttc_contract_plan_destroy
+
     def __del__(self):
         if getattr(self, "handle", None):
-            _lib.ttc_contract_plan_destroy(self.handle)
+            type(self)._destroy(self.handle)
             self.handle = None
 
 
