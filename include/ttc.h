@@ -203,9 +203,10 @@ ttc_status ttc_reconstruct_ws(const ttc_tt_batch* t, const int32_t* perm, float*
  *   rounding.  The library allocates nothing.
  * Tensors of prod(dims) <= 16384 with every unfolding's smaller side <= 64 are held in shared memory (the two
  * paths above).  Larger ones (Example 2's 20 x 20 x 20 x 5 and 20 x 20 x 20 x 5 x 4) take a
- * one-sided Jacobi kernel over the workspace, which is then REQUIRED (8 (2 prod(dims) + gmax^2 + 16) bytes per
- * tensor, gmax the largest smaller side; NULL / too small: TTC_ERR_ARG naming the size); limits prod(dims) <= 2^27
- * and gmax <= 1024 (else TTC_ERR_UNSUPPORTED).  eps < 0: TTC_ERR_ARG.
+ * one-sided Jacobi kernel over the workspace, which is then REQUIRED (8 (2 prod(dims) + gmax^2 + 2 gmax + 80)
+ * + 128 bytes per tensor, gmax the largest smaller side; NULL / too small: TTC_ERR_ARG naming the size); a group
+ * of co-resident CTAs per tensor (cooperative launches, chunked when the batch exceeds the resident CTAs); limits
+ * prod(dims) <= 2^27 and gmax <= 1024 (else TTC_ERR_UNSUPPORTED).  eps < 0: TTC_ERR_ARG.
  * ------------------------------------------------------------------------------------------------- */
 ttc_status ttc_tt_svd_capacity(int32_t order, const int32_t* dims, const int32_t* perm, int64_t* train_cap);
 ttc_status ttc_tt_svd_workspace(int32_t batch, int32_t order, const int32_t* dims, const int32_t* perm,

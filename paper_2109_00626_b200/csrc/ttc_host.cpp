@@ -589,7 +589,7 @@ ttc_status ttc_tt_svd_workspace(int32_t batch, int32_t order, const int32_t* dim
     int64_t total = 1, off[6];
     for (int n = 0; n < order; ++n) total *= rd[n];
     if (ttsvd_needs_big(total, gmax)) {
-        *workspace_bytes = 8 * (int64_t)batch * ttc::ttsvd_big_ws_per((int32_t)total, gmax);
+        *workspace_bytes = ttc::ttsvd_big_ws_bytes(batch, (int32_t)total, gmax);
         return TTC_OK;
     }
     *workspace_bytes = (order >= 2 && gmax <= 32) ? ttsvd_ws_layout(batch, total, gmax, off) : 0;
@@ -627,13 +627,13 @@ ttc_status ttc_tt_svd(int32_t batch, int32_t order, const int32_t* dims, const f
     const int64_t g = gmax;
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     if (ttsvd_needs_big(total, gmax)) {   // one-sided Jacobi over the caller's fp64 workspace (ttsvd_big.cu)
-        const int64_t need = 8 * (int64_t)batch * ttc::ttsvd_big_ws_per((int32_t)total, gmax);
+        const int64_t need = ttc::ttsvd_big_ws_bytes(batch, (int32_t)total, gmax);
         if (!workspace_dev || workspace_bytes < need)
             return fail(TTC_ERR_ARG, "tensors of %lld elements (largest unfolding side %d) need a workspace of %lld bytes "
                         "(ttc_tt_svd_workspace), got %lld", (long long)total, gmax, (long long)need,
                         (long long)workspace_bytes);
         if (reinterpret_cast<uintptr_t>(workspace_dev) & 7u) return fail(TTC_ERR_ALIGN, "workspace_dev not 8-byte aligned");
-        const cudaError_t e = ttc::launch_ttsvd_big(a, static_cast<double*>(workspace_dev), cs);
+        const cudaError_t e = ttc::launch_ttsvd_big(a, workspace_dev, cs);
         if (e != cudaSuccess) return cuda_fail(e, "ttc_tt_svd launch");
         return TTC_OK;
     }

@@ -165,7 +165,7 @@ cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStre
 // tensors beyond the shared-memory kernels (ttsvd_big.cu): one CTA per tensor over an fp64 workspace of
 // ttsvd_big_ws_per(elems, gmax) doubles per tensor; every unfolding's smaller side <= kTtsvdBigMaxSide
 constexpr int kTtsvdBigMaxSide = 1024;
-int64_t     ttsvd_big_ws_per(int32_t elems, int32_t gmax);
-cudaError_t launch_ttsvd_big(const TtsvdArgs& a, double* ws, cudaStream_t s);
+int64_t     ttsvd_big_ws_bytes(int32_t B, int32_t elems, int32_t gmax);
+cudaError_t launch_ttsvd_big(const TtsvdArgs& a, void* workspace, cudaStream_t s);
 
 }  // namespace ttc

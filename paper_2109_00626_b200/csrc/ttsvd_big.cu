@@ -1,21 +1,25 @@
 // ttsvd_big.cu -- TT-SVD (Alg. 1) of tensors too large for the shared-memory kernels of
 // ttsvd.cu (more than 16,384 elements, or an unfolding whose smaller side exceeds 64: Example 2's cases (ii)
 // 20 x 20 x 20 x 5 and (iii) 20 x 20 x 20 x 5 x 4, whose middle unfoldings are 400 x 100 and
-// 400 x 400).  One CTA per tensor over a caller-owned fp64 workspace (ttc_tt_svd_workspace).
+// 400 x 400), over a caller-owned fp64 workspace (ttc_tt_svd_workspace).
 //
 // Each step n factors the unfolding Z (m x c, column-major: the Eq. 2 order of the remaining modes) by ONE-SIDED
 // Jacobi (Hestenes) on the matrix A whose s = min(m, c) columns are orthogonalised:
 //   m <= c:  A = Z^T (c x m).  A V has orthogonal columns  =>  V = U (left singular vectors of Z) and
 //            (A V)^T = U^T Z = S V'^T, the next unfolding, directly.
 //   m >  c:  A = Z   (m x c).  Z V = U S  =>  U = columns of Z V / sigma, next unfolding S V^T.
-// Rotations of column pairs in the parallel round-robin order (one warp per pair, s/2 pairs per round), until a
-// sweep rotates nothing (|a_p . a_q| <= 1e-15 sqrt(|a_p|^2 |a_q|^2)); singular values = norms of A V's columns.
-// The delta-truncated rank, the 1e-7 singular-value floor (R25) and the sign convention (R24: the largest-magnitude
-// entry of every left singular vector positive, the matching row of S V^T flipped with it) are Alg. 1's as the
-// oracle reads them (oracle/ttsvd.py).  Alg. 2 step 1's permutation is folded into the first read.
+// Rotations of column pairs in the parallel round-robin order, until a sweep rotates nothing
+// (|a_p . a_q| <= 1e-15 sqrt(|a_p|^2 |a_q|^2)); singular values = norms of A V's columns.  The delta-truncated
+// rank, the 1e-7 singular-value floor (R25) and the sign convention (R24: the largest-magnitude entry of every
+// left singular vector positive, the matching row of S V^T flipped with it) are Alg. 1's as the oracle reads
+// them (oracle/ttsvd.py).  Alg. 2 step 1's permutation is folded into the first read.
 //
-// Every pass over A and V goes through L2 / HBM (a 400 x 400 fp64 A is 1.25 MB): this path is for the paper's
-// Example 2 sizes, not a hot loop.
+// Parallelism: a GROUP of C co-resident CTAs per tensor (cooperative launch), synchronised by a per-tensor
+// counter barrier in the workspace.  The s/2 rotations of a round are independent: one warp per column pair
+// when the columns are short, one CTA per pair (block reductions) when they are long (L >= 2048, e.g. the
+// 8,000-long columns of case (iii)'s first unfolding).  Every reduction is in a fixed order, so the result does
+// not depend on C.  A, V and Z live in L2 / HBM (a 400 x 400 fp64 A is 1.25 MB).
+#include <algorithm>
 #include <cmath>
 
 #include "ttc_internal.h"
@@ -27,6 +31,9 @@ constexpr int kBigThreads = 512;
 constexpr int kBigWarps = kBigThreads / 32;
 constexpr double kSigmaFloor = 1e-7;   // R25
 constexpr int kMaxSweeps = 60;
+constexpr int kMaxGroup = 64;          // CTAs per tensor
+constexpr int kSyncInts = 32;          // per tensor: barrier counter, rotation counter (128 bytes apart)
+constexpr int kCtaPairL = 2048;        // columns at least this long: one CTA per pair
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -34,27 +41,67 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+__device__ __forceinline__ unsigned ld_acquire(const int* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Barrier of the C CTAs of one tensor: a monotone arrival counter (zeroed by the host before the launch).
+__device__ __forceinline__ void group_barrier(int* cnt, unsigned& target, int C) {
+    __syncthreads();
+    target += (unsigned)C;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(cnt, 1);
+        while (ld_acquire(cnt) < target) __nanosleep(32);
+    }
+    __syncthreads();
+}
+
 // round-robin tournament: the player at position pos in round r (position 0 fixed, the others rotate)
 __device__ __forceinline__ int rr_player(int pos, int r, int S) { return pos == 0 ? 0 : ((pos - 1 + r) % (S - 1)) + 1; }
 
-__global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs a, double* ws, int64_t ws_per) {
+// Jacobi rotation of columns (ap, aq) given their Gram entries; false when already orthogonal
+__device__ __forceinline__ bool rotation(double al, double be, double ga, double& cs, double& sn) {
+    if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) return false;
+    const double zeta = (be - al) / (2.0 * ga);
+    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    cs = 1.0 / sqrt(1.0 + t * t);
+    sn = cs * t;
+    return true;
+}
+
+__global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs a, double* ws, int* sync,
+                                                               int64_t ws_per, int C, int b0) {
     __shared__ double sig[kTtsvdBigMaxSide];
     __shared__ int ord[kTtsvdBigMaxSide];
-    __shared__ double sgn[kTtsvdBigMaxSide];
-    __shared__ double red[kBigWarps];
-    __shared__ int rotated, rank_s;
-    const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int N = a.N, elems = a.elems;
+    __shared__ double red[3][kBigWarps];
+    __shared__ double bc[4];
+    __shared__ int rank_s, rot_any, rot_now;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = blockIdx.x / C, cg = blockIdx.x - g * C;   // tensor of the chunk, CTA within its group
+    const int b = b0 + g;
+    if (b >= a.B) return;   // whole groups only: every CTA of a group takes this branch or none does
+    const int N = a.N, elems = a.elems, gmax = a.gmax;
     double* Z = ws + (int64_t)b * ws_per;   // current unfolding, column-major
     double* A = Z + elems;                  // the matrix whose columns are orthogonalised
     double* V = A + elems;                  // accumulated rotations (s x s)
+    double* sig_g = V + (int64_t)gmax * gmax;
+    double* sgn_g = sig_g + gmax;
+    double* part = sgn_g + gmax;            // kMaxGroup partial norms
+    int* cnt = sync + (int64_t)b * kSyncInts;
+    int* rot = cnt + 16;
+    unsigned target = 0;
     const float* src = a.dense + (int64_t)b * elems;
     float* core = a.cores + (int64_t)b * a.train_cap;
     int32_t* rk = a.ranks + (int64_t)b * (N + 1);
+    const int gt = cg * kBigThreads + tid, gts = C * kBigThreads;   // thread index / count in the group
+    const int gw = cg * kBigWarps + warp, gws = C * kBigWarps;      // warp index / count in the group
 
-    // ---- Z_0 = X^rho (Alg. 2 step 1's permutation folded into the gather), ||X||^2
+    // ---- Z_0 = X^rho (Alg. 2 step 1's permutation folded into the gather), ||X||^2 (fixed-order partials)
     double nrm = 0.0;
-    for (int e = tid; e < elems; e += kBigThreads) {
+    for (int e = gt; e < elems; e += gts) {
         int q = e;
         int64_t off = 0;
         for (int k = 0; k < N; ++k) {
@@ -67,86 +114,141 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
         nrm += v * v;
     }
     nrm = warp_sum(nrm);
-    if (lane == 0) red[warp] = nrm;
+    if (lane == 0) red[0][warp] = nrm;
     __syncthreads();
     if (tid == 0) {
         double t = 0.0;
-        for (int w = 0; w < kBigWarps; ++w) t += red[w];
-        red[0] = t;
-        rk[0] = 1;
-        rk[N] = 1;
+        for (int w = 0; w < kBigWarps; ++w) t += red[0][w];
+        part[cg] = t;
+    }
+    group_barrier(cnt, target, C);
+    if (tid == 0) {
+        double t = 0.0;
+        for (int k = 0; k < C; ++k) t += part[k];
+        bc[0] = t;
+        if (cg == 0) {
+            rk[0] = 1;
+            rk[N] = 1;
+        }
     }
     __syncthreads();
-    const double delta2 = a.eps2 * red[0];   // (eps / sqrt(N - 1))^2 ||X||^2
-    __syncthreads();
+    const double delta2 = a.eps2 * bc[0];   // (eps / sqrt(N - 1))^2 ||X||^2
 
     int Rp = 1;                 // R_{n-1}
     int64_t cur = elems;        // elements of the current unfolding
     int64_t coff = 0;           // offset of core n in the train
+    int rot_seen = 0;           // the rotation counter after the previous sweep (the same in every CTA)
     for (int n = 0; n + 1 < N; ++n) {
         const int m = Rp * a.dims[n];
         const int c = (int)(cur / m);
         const bool wide = m <= c;            // A = Z^T
         const int s = wide ? m : c, L = wide ? c : m;
         // A (L x s, column-major) and V = I (s x s)
-        for (int64_t e = tid; e < (int64_t)L * s; e += kBigThreads) {
+        for (int64_t e = gt; e < (int64_t)L * s; e += gts) {
             const int row = (int)(e % L), col = (int)(e / L);
             A[e] = wide ? Z[col + (int64_t)m * row] : Z[e];
         }
-        for (int64_t e = tid; e < (int64_t)s * s; e += kBigThreads) V[e] = (e % s) == (e / s) ? 1.0 : 0.0;
-        __syncthreads();
+        for (int64_t e = gt; e < (int64_t)s * s; e += gts) V[e] = (e % s) == (e / s) ? 1.0 : 0.0;
+        group_barrier(cnt, target, C);
         // ---- one-sided Jacobi sweeps
         const int S = s + (s & 1);
+        const bool cta_pairs = L >= kCtaPairL;
         for (int sweep = 0; sweep < kMaxSweeps && s > 1; ++sweep) {
-            if (tid == 0) rotated = 0;
+            if (tid == 0) rot_any = 0;
             __syncthreads();
             for (int r = 0; r < S - 1; ++r) {
-                for (int k = warp; k < S / 2; k += kBigWarps) {
-                    const int p = rr_player(k, r, S), q = rr_player(S - 1 - k, r, S);
-                    if (p >= s || q >= s) continue;
-                    double* ap = A + (int64_t)L * p;
-                    double* aq = A + (int64_t)L * q;
-                    double al = 0.0, be = 0.0, ga = 0.0;
-                    for (int e = lane; e < L; e += 32) {
-                        const double x = ap[e], y = aq[e];
-                        al = fma(x, x, al);
-                        be = fma(y, y, be);
-                        ga = fma(x, y, ga);
+                if (cta_pairs) {
+                    for (int k = cg; k < S / 2; k += C) {
+                        const int p = rr_player(k, r, S), q = rr_player(S - 1 - k, r, S);
+                        if (p >= s || q >= s) continue;
+                        double* ap = A + (int64_t)L * p;
+                        double* aq = A + (int64_t)L * q;
+                        double al = 0.0, be = 0.0, ga = 0.0;
+                        for (int e = tid; e < L; e += kBigThreads) {
+                            const double x = ap[e], y = aq[e];
+                            al = fma(x, x, al);
+                            be = fma(y, y, be);
+                            ga = fma(x, y, ga);
+                        }
+                        al = warp_sum(al);
+                        be = warp_sum(be);
+                        ga = warp_sum(ga);
+                        if (lane == 0) { red[0][warp] = al; red[1][warp] = be; red[2][warp] = ga; }
+                        __syncthreads();
+                        al = be = ga = 0.0;
+                        for (int w = 0; w < kBigWarps; ++w) { al += red[0][w]; be += red[1][w]; ga += red[2][w]; }
+                        __syncthreads();   // red is reused by the next pair
+                        double cs, sn;
+                        if (!rotation(al, be, ga, cs, sn)) continue;   // uniform over the CTA
+                        for (int e = tid; e < L; e += kBigThreads) {
+                            const double x = ap[e], y = aq[e];
+                            ap[e] = cs * x - sn * y;
+                            aq[e] = sn * x + cs * y;
+                        }
+                        double* vp = V + (int64_t)s * p;
+                        double* vq = V + (int64_t)s * q;
+                        for (int e = tid; e < s; e += kBigThreads) {
+                            const double x = vp[e], y = vq[e];
+                            vp[e] = cs * x - sn * y;
+                            vq[e] = sn * x + cs * y;
+                        }
+                        if (tid == 0) rot_any = 1;
                     }
-                    al = warp_sum(al);
-                    be = warp_sum(be);
-                    ga = warp_sum(ga);
-                    if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
-                    const double zeta = (be - al) / (2.0 * ga);
-                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-                    for (int e = lane; e < L; e += 32) {
-                        const double x = ap[e], y = aq[e];
-                        ap[e] = cs * x - sn * y;
-                        aq[e] = sn * x + cs * y;
+                } else {
+                    for (int k = gw; k < S / 2; k += gws) {
+                        const int p = rr_player(k, r, S), q = rr_player(S - 1 - k, r, S);
+                        if (p >= s || q >= s) continue;
+                        double* ap = A + (int64_t)L * p;
+                        double* aq = A + (int64_t)L * q;
+                        double al = 0.0, be = 0.0, ga = 0.0;
+                        for (int e = lane; e < L; e += 32) {
+                            const double x = ap[e], y = aq[e];
+                            al = fma(x, x, al);
+                            be = fma(y, y, be);
+                            ga = fma(x, y, ga);
+                        }
+                        al = warp_sum(al);
+                        be = warp_sum(be);
+                        ga = warp_sum(ga);
+                        double cs, sn;
+                        if (!rotation(al, be, ga, cs, sn)) continue;
+                        for (int e = lane; e < L; e += 32) {
+                            const double x = ap[e], y = aq[e];
+                            ap[e] = cs * x - sn * y;
+                            aq[e] = sn * x + cs * y;
+                        }
+                        double* vp = V + (int64_t)s * p;
+                        double* vq = V + (int64_t)s * q;
+                        for (int e = lane; e < s; e += 32) {
+                            const double x = vp[e], y = vq[e];
+                            vp[e] = cs * x - sn * y;
+                            vq[e] = sn * x + cs * y;
+                        }
+                        if (lane == 0) rot_any = 1;
                     }
-                    double* vp = V + (int64_t)s * p;
-                    double* vq = V + (int64_t)s * q;
-                    for (int e = lane; e < s; e += 32) {
-                        const double x = vp[e], y = vq[e];
-                        vp[e] = cs * x - sn * y;
-                        vq[e] = sn * x + cs * y;
-                    }
-                    if (lane == 0) rotated = 1;
                 }
-                __syncthreads();
+                if (r == S - 2) {   // count the CTAs that rotated this sweep (monotone counter)
+                    __syncthreads();
+                    if (tid == 0 && rot_any) atomicAdd(rot, 1);
+                }
+                group_barrier(cnt, target, C);
             }
-            if (!rotated) break;
-            __syncthreads();
+            if (tid == 0) rot_now = (int)ld_acquire(rot);
+            group_barrier(cnt, target, C);   // every CTA has read the count before the next sweep adds to it
+            const int now = rot_now;
+            if (now == rot_seen) break;      // a sweep without a rotation: converged
+            rot_seen = now;
         }
-        // ---- singular values (column norms), descending order (ties: lower index first)
-        for (int j = warp; j < s; j += kBigWarps) {
+        // ---- singular values (column norms) -> sig_g; every CTA then sorts them itself (same order everywhere)
+        for (int j = gw; j < s; j += gws) {
             const double* aj = A + (int64_t)L * j;
             double v = 0.0;
             for (int e = lane; e < L; e += 32) v = fma(aj[e], aj[e], v);
             v = warp_sum(v);
-            if (lane == 0) sig[j] = sqrt(v);
+            if (lane == 0) sig_g[j] = sqrt(v);
         }
+        group_barrier(cnt, target, C);
+        for (int j = tid; j < s; j += kBigThreads) sig[j] = sig_g[j];
         __syncthreads();
         for (int j = tid; j < s; j += kBigThreads) {
             int pos = 0;
@@ -174,12 +276,12 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                 }
             }
             rank_s = R;
-            rk[n + 1] = R;
+            if (cg == 0) rk[n + 1] = R;
         }
         __syncthreads();
         const int R = rank_s;
         // ---- core n = U (m x R) with the sign convention: column k is V[:, ord[k]] (wide) or A[:, ord[k]] / sigma
-        for (int k = warp; k < R; k += kBigWarps) {
+        for (int k = gw; k < R; k += gws) {
             const int j = ord[k];
             const double inv = wide ? 1.0 : (sig[j] > 0.0 ? 1.0 / sig[j] : 0.0);
             const double* u = wide ? V + (int64_t)s * j : A + (int64_t)L * j;
@@ -196,34 +298,62 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                 if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
             }
             const double sg = u[bi] < 0.0 ? -1.0 : 1.0;
-            if (lane == 0) sgn[k] = sg;
+            if (lane == 0) sgn_g[k] = sg;
             for (int e = lane; e < m; e += 32) core[coff + e + (int64_t)m * k] = (float)(sg * inv * u[e]);
         }
-        __syncthreads();
+        group_barrier(cnt, target, C);
         // ---- next unfolding Z' = S V^T (R x c, column-major), reshaped to (R I_{n+1}) x rest by the index order
-        for (int64_t e = tid; e < (int64_t)R * c; e += kBigThreads) {
+        for (int64_t e = gt; e < (int64_t)R * c; e += gts) {
             const int k = (int)(e % R), col = (int)(e / R);
             const int j = ord[k];
-            Z[e] = wide ? sgn[k] * A[col + (int64_t)L * j] : sgn[k] * sig[j] * V[col + (int64_t)s * j];
+            Z[e] = wide ? sgn_g[k] * A[col + (int64_t)L * j] : sgn_g[k] * sig[j] * V[col + (int64_t)s * j];
         }
-        __syncthreads();
+        group_barrier(cnt, target, C);
         coff += (int64_t)m * R;
         Rp = R;
         cur = (int64_t)R * c;
     }
     // ---- last core: G^(N) = Z (R_{N-1} x I_N x 1)
-    for (int64_t e = tid; e < cur; e += kBigThreads) core[coff + e] = (float)Z[e];
+    for (int64_t e = gt; e < cur; e += gts) core[coff + e] = (float)Z[e];
 }
 
 }  // namespace
 
-int64_t ttsvd_big_ws_per(int32_t elems, int32_t gmax) {
-    return 2 * (int64_t)elems + (int64_t)gmax * gmax + 16;   // doubles per tensor: Z, A, V (+ padding)
+int64_t ttsvd_big_ws_bytes(int32_t B, int32_t elems, int32_t gmax) {
+    // per tensor: Z, A (elems doubles each), V (gmax^2), sig and signs (gmax each), group partials; plus the
+    // per-tensor synchronisation ints (zeroed by every launch)
+    const int64_t per = 2 * (int64_t)elems + (int64_t)gmax * gmax + 2 * (int64_t)gmax + kMaxGroup + 16;
+    return 8 * (int64_t)B * per + 4 * (int64_t)B * kSyncInts;
 }
 
-cudaError_t launch_ttsvd_big(const TtsvdArgs& a, double* ws, cudaStream_t s) {
-    ttsvd_big_kernel<<<a.B, kBigThreads, 0, s>>>(a, ws, ttsvd_big_ws_per(a.elems, a.gmax));
-    return cudaGetLastError();
+cudaError_t launch_ttsvd_big(const TtsvdArgs& a, void* workspace, cudaStream_t s) {
+    if (a.B <= 0) return cudaSuccess;
+    const int64_t per = 2 * (int64_t)a.elems + (int64_t)a.gmax * a.gmax + 2 * (int64_t)a.gmax + kMaxGroup + 16;
+    double* ws = static_cast<double*>(workspace);
+    int* sync = reinterpret_cast<int*>(ws + (int64_t)a.B * per);
+    cudaError_t e = cudaMemsetAsync(sync, 0, 4 * (size_t)a.B * kSyncInts, s);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, occ = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttsvd_big_kernel, kBigThreads, 0)) != cudaSuccess)
+        return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const int slots = sms * occ;
+    // CTAs per tensor: as many as the co-resident slots allow for the whole batch (at most kMaxGroup); batches
+    // larger than the slots run in chunks of whole groups
+    const int C = std::max(1, std::min(kMaxGroup, slots / a.B));
+    const int per_launch = std::max(1, slots / C);
+    for (int b0 = 0; b0 < a.B; b0 += per_launch) {
+        const int groups = std::min(per_launch, a.B - b0);
+        TtsvdArgs aa = a;
+        int64_t wp = per;
+        int Cc = C, bb = b0;
+        void* args[] = {&aa, &ws, &sync, &wp, &Cc, &bb};
+        e = cudaLaunchCooperativeKernel((const void*)ttsvd_big_kernel, dim3(groups * C), dim3(kBigThreads), args, 0, s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace ttc

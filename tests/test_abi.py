@@ -289,12 +289,15 @@ def test_tt_svd_workspace_sizes():
     assert ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(2, 1)) > 0
     with pytest.raises(ttc.TTCError):
         ttc.ttc_tt_svd_workspace(B, (4, 6), perm=(1, 1))
-    # beyond shared memory (Example 2's (ii) / (iii)): the one-sided Jacobi kernel's fp64 Z, A (prod(dims) each)
-    # and V (gmax^2) per tensor, gmax = the largest smaller side of an unfolding (400 x 100 -> 100; 400 x 400 -> 400)
-    assert ttc.ttc_tt_svd_workspace(B, (20, 20, 20, 5)) == 8 * B * (2 * 40000 + 100 * 100 + 16)
-    assert ttc.ttc_tt_svd_workspace(B, (20, 20, 20, 5, 4)) == 8 * B * (2 * 160000 + 400 * 400 + 16)
-    assert ttc.ttc_tt_svd_workspace(B, (5, 20, 20, 20), perm=(2, 3, 4, 1)) == 8 * B * (2 * 40000 + 100 * 100 + 16)
-    assert ttc.ttc_tt_svd_workspace(B, (70, 70)) == 8 * B * (2 * 4900 + 70 * 70 + 16)   # side 70 > 64
+    # beyond shared memory (Example 2's (ii) / (iii)): the one-sided Jacobi kernel's fp64 Z, A (prod(dims) each),
+    # V (gmax^2), singular values and signs (gmax each) and 64 + 16 doubles of group partials / padding per tensor,
+    # plus 32 synchronisation ints per tensor; gmax = the largest smaller side of an unfolding (400 x 100 -> 100;
+    # 400 x 400 -> 400)
+    big = lambda el, g: 8 * B * (2 * el + g * g + 2 * g + 80) + 4 * B * 32
+    assert ttc.ttc_tt_svd_workspace(B, (20, 20, 20, 5)) == big(40000, 100)
+    assert ttc.ttc_tt_svd_workspace(B, (20, 20, 20, 5, 4)) == big(160000, 400)
+    assert ttc.ttc_tt_svd_workspace(B, (5, 20, 20, 20), perm=(2, 3, 4, 1)) == big(40000, 100)
+    assert ttc.ttc_tt_svd_workspace(B, (70, 70)) == big(4900, 70)   # side 70 > 64
     with pytest.raises(ttc.TTCError) as e:
         ttc.ttc_tt_svd_workspace(B, (2000, 2000))            # smaller side 2000 > 1024
     assert e.value.status == ttc.TTC_ERR_UNSUPPORTED
