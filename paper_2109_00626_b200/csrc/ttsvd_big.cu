@@ -34,6 +34,7 @@ constexpr int kMaxSweeps = 60;
 constexpr int kMaxGroup = 64;          // CTAs per tensor
 constexpr int kSyncInts = 32;          // per tensor: barrier counter, rotation counter (128 bytes apart)
 constexpr int kCtaPairL = 2048;        // columns at least this long: one CTA per pair
+constexpr int kRegCol = 16;            // warp-per-pair columns up to 32 kRegCol long are held in registers
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -54,7 +55,8 @@ __device__ __forceinline__ void group_barrier(int* cnt, unsigned& target, int C)
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(cnt, 1);
-        while (ld_acquire(cnt) < target) __nanosleep(32);
+        while (ld_acquire(cnt) < target) {
+        }
     }
     __syncthreads();
 }
@@ -201,21 +203,49 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                         double* ap = A + (int64_t)L * p;
                         double* aq = A + (int64_t)L * q;
                         double al = 0.0, be = 0.0, ga = 0.0;
-                        for (int e = lane; e < L; e += 32) {
-                            const double x = ap[e], y = aq[e];
-                            al = fma(x, x, al);
-                            be = fma(y, y, be);
-                            ga = fma(x, y, ga);
-                        }
-                        al = warp_sum(al);
-                        be = warp_sum(be);
-                        ga = warp_sum(ga);
                         double cs, sn;
-                        if (!rotation(al, be, ga, cs, sn)) continue;
-                        for (int e = lane; e < L; e += 32) {
-                            const double x = ap[e], y = aq[e];
-                            ap[e] = cs * x - sn * y;
-                            aq[e] = sn * x + cs * y;
+                        if (L <= 32 * kRegCol) {   // both columns in registers: one load of each element
+                            double xr[kRegCol], yr[kRegCol];
+#pragma unroll
+                            for (int t = 0; t < kRegCol; ++t) {
+                                const int e = lane + 32 * t;
+                                xr[t] = e < L ? ap[e] : 0.0;
+                                yr[t] = e < L ? aq[e] : 0.0;
+                            }
+#pragma unroll
+                            for (int t = 0; t < kRegCol; ++t) {
+                                al = fma(xr[t], xr[t], al);
+                                be = fma(yr[t], yr[t], be);
+                                ga = fma(xr[t], yr[t], ga);
+                            }
+                            al = warp_sum(al);
+                            be = warp_sum(be);
+                            ga = warp_sum(ga);
+                            if (!rotation(al, be, ga, cs, sn)) continue;
+#pragma unroll
+                            for (int t = 0; t < kRegCol; ++t) {
+                                const int e = lane + 32 * t;
+                                if (e < L) {
+                                    ap[e] = cs * xr[t] - sn * yr[t];
+                                    aq[e] = sn * xr[t] + cs * yr[t];
+                                }
+                            }
+                        } else {
+                            for (int e = lane; e < L; e += 32) {
+                                const double x = ap[e], y = aq[e];
+                                al = fma(x, x, al);
+                                be = fma(y, y, be);
+                                ga = fma(x, y, ga);
+                            }
+                            al = warp_sum(al);
+                            be = warp_sum(be);
+                            ga = warp_sum(ga);
+                            if (!rotation(al, be, ga, cs, sn)) continue;
+                            for (int e = lane; e < L; e += 32) {
+                                const double x = ap[e], y = aq[e];
+                                ap[e] = cs * x - sn * y;
+                                aq[e] = sn * x + cs * y;
+                            }
                         }
                         double* vp = V + (int64_t)s * p;
                         double* vq = V + (int64_t)s * q;
