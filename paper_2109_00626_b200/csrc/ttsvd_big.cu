@@ -35,6 +35,9 @@ constexpr int kMaxGroup = 64;          // CTAs per tensor
 constexpr int kSyncInts = 32;          // per tensor: barrier counter, rotation counter (128 bytes apart)
 constexpr int kCtaPairL = 2048;        // columns at least this long: one CTA per pair
 constexpr int kRegCol = 16;            // warp-per-pair columns up to 32 kRegCol long are held in registers
+constexpr int kMaxBlk2 = 32;           // block mode: at most 2 x 16 columns per block pair
+constexpr int kLocalSweeps = 1;        // block mode: full local sweeps in a sweep's first block round
+constexpr int kDynBytes = 200 * 1024;  // block mode: dynamic shared memory per CTA
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -75,12 +78,13 @@ __device__ __forceinline__ bool rotation(double al, double be, double ga, double
 }
 
 __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs a, double* ws, int* sync,
-                                                               int64_t ws_per, int C, int b0) {
+                                                               int64_t ws_per, int C, int b0, int dyn_doubles) {
     __shared__ double sig[kTtsvdBigMaxSide];
     __shared__ int ord[kTtsvdBigMaxSide];
     __shared__ double red[3][kBigWarps];
     __shared__ double bc[4];
-    __shared__ int rank_s, rot_any, rot_now;
+    __shared__ int rank_s, rot_any, rot_now, lrot, lrot_any;
+    extern __shared__ double dsm[];   // block mode: two column blocks of A and their rotation matrix
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = blockIdx.x / C, cg = blockIdx.x - g * C;   // tensor of the chunk, CTA within its group
     const int b = b0 + g;
@@ -155,7 +159,128 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
         // ---- one-sided Jacobi sweeps
         const int S = s + (s & 1);
         const bool cta_pairs = L >= kCtaPairL;
-        for (int sweep = 0; sweep < kMaxSweeps && s > 1; ++sweep) {
+        int bs = 16;   // block mode: columns per block (two blocks and their rotation matrix in shared memory)
+        while (bs > 4 && (int64_t)L * 2 * bs + 4 * bs * bs > dyn_doubles) bs >>= 1;
+        const bool block_mode = !cta_pairs && s >= 32 && (int64_t)L * 2 * bs + 4 * bs * bs <= dyn_doubles;
+        if (block_mode) {
+            // Block one-sided Jacobi: the s columns in nb blocks of bs, block pairs in the round-robin order (one
+            // CTA per block pair, nb - 1 group barriers per sweep instead of s - 1); a block pair is loaded into
+            // shared memory and orthogonalised there by local round-robin sweeps (warp per column pair), its
+            // rotations accumulated in a 2bs x 2bs matrix Q and applied to V's columns once: V_pair <- V_pair Q.
+            const int nb0 = (s + bs - 1) / bs, nb = nb0 + (nb0 & 1);
+            const int ldq = 2 * bs;
+            double* As = dsm;                             // nl columns of L doubles
+            double* Qm = dsm + (int64_t)L * 2 * bs;       // nl x nl, column-major, leading dimension 2 bs
+            for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+                if (tid == 0) rot_any = 0;
+                __syncthreads();
+                for (int r = 0; r < nb - 1; ++r) {
+                    for (int k = cg; k < nb / 2; k += C) {
+                        const int P = rr_player(k, r, nb), Qb = rr_player(nb - 1 - k, r, nb);
+                        const int p0 = P * bs, np = max(0, min(bs, s - p0));
+                        const int q0 = Qb * bs, nq = max(0, min(bs, s - q0));
+                        const int nl = np + nq;
+                        if (nl < 2) continue;
+                        for (int e = tid; e < nl * L; e += kBigThreads) {
+                            const int j = e / L, i = e - j * L;
+                            As[e] = A[(int64_t)L * (j < np ? p0 + j : q0 + j - np) + i];
+                        }
+                        for (int e = tid; e < ldq * ldq; e += kBigThreads) Qm[e] = (e % ldq) == (e / ldq) ? 1.0 : 0.0;
+                        if (tid == 0) lrot_any = 0;
+                        __syncthreads();
+                        // the sweep's first block round pairs every block once: a full local sweep there covers
+                        // the pairs inside the blocks; later rounds only the np x nq cross pairs (Latin square:
+                        // round t pairs local column i with np + (i + t) mod M, M = max(np, nq))
+                        const bool full = r == 0;
+                        const int S2 = nl + (nl & 1), M = max(np, nq);
+                        const int nrl = full ? S2 - 1 : M;
+                        for (int ls = 0; ls < (full ? kLocalSweeps : 1); ++ls) {
+                            if (tid == 0) lrot = 0;
+                            __syncthreads();
+                            for (int rl = 0; rl < nrl; ++rl) {
+                                if (warp < (full ? S2 / 2 : np)) {
+                                    int pa, qa;
+                                    if (full) {
+                                        pa = rr_player(warp, rl, S2);
+                                        qa = rr_player(S2 - 1 - warp, rl, S2);
+                                    } else {
+                                        pa = warp;
+                                        const int jq = (warp + rl) % M;
+                                        qa = jq < nq ? np + jq : nl;   // nl: no partner this round
+                                    }
+                                    if (pa < nl && qa < nl) {
+                                        double* x = As + (int64_t)L * pa;
+                                        double* y = As + (int64_t)L * qa;
+                                        double al = 0.0, be = 0.0, ga = 0.0;
+                                        for (int e = lane; e < L; e += 32) {
+                                            const double xv = x[e], yv = y[e];
+                                            al = fma(xv, xv, al);
+                                            be = fma(yv, yv, be);
+                                            ga = fma(xv, yv, ga);
+                                        }
+                                        al = warp_sum(al);
+                                        be = warp_sum(be);
+                                        ga = warp_sum(ga);
+                                        double cs, sn;
+                                        if (rotation(al, be, ga, cs, sn)) {
+                                            for (int e = lane; e < L; e += 32) {
+                                                const double xv = x[e], yv = y[e];
+                                                x[e] = cs * xv - sn * yv;
+                                                y[e] = sn * xv + cs * yv;
+                                            }
+                                            if (lane < nl) {
+                                                const double xv = Qm[lane + ldq * pa], yv = Qm[lane + ldq * qa];
+                                                Qm[lane + ldq * pa] = cs * xv - sn * yv;
+                                                Qm[lane + ldq * qa] = sn * xv + cs * yv;
+                                            }
+                                            if (lane == 0) lrot = 1;
+                                        }
+                                    }
+                                }
+                                __syncthreads();
+                            }
+                            const int lr = lrot;
+                            __syncthreads();   // every thread has read lrot before it is reset
+                            if (!lr) break;
+                            if (tid == 0) lrot_any = 1;
+                        }
+                        __syncthreads();
+                        if (lrot_any) {   // uniform: write the pair back, V's columns times Q
+                            for (int e = tid; e < nl * L; e += kBigThreads) {
+                                const int j = e / L, i = e - j * L;
+                                A[(int64_t)L * (j < np ? p0 + j : q0 + j - np) + i] = As[e];
+                            }
+                            for (int e = tid; e < s; e += kBigThreads) {
+                                double vr[kMaxBlk2];
+#pragma unroll
+                                for (int j = 0; j < kMaxBlk2; ++j)
+                                    vr[j] = j < nl ? V[e + (int64_t)s * (j < np ? p0 + j : q0 + j - np)] : 0.0;
+#pragma unroll 4
+                                for (int j = 0; j < nl; ++j) {
+                                    double o = 0.0;
+#pragma unroll
+                                    for (int i = 0; i < kMaxBlk2; ++i) o = fma(vr[i], Qm[i + ldq * j], o);
+                                    V[e + (int64_t)s * (j < np ? p0 + j : q0 + j - np)] = o;
+                                }
+                            }
+                            if (tid == 0) rot_any = 1;
+                        }
+                        __syncthreads();   // shared memory is reused by the next block pair
+                    }
+                    if (r == nb - 2) {
+                        __syncthreads();
+                        if (tid == 0 && rot_any) atomicAdd(rot, 1);
+                    }
+                    group_barrier(cnt, target, C);
+                }
+                if (tid == 0) rot_now = (int)ld_acquire(rot);
+                group_barrier(cnt, target, C);
+                const int now = rot_now;
+                if (now == rot_seen) break;
+                rot_seen = now;
+            }
+        }
+        for (int sweep = 0; sweep < kMaxSweeps && s > 1 && !block_mode; ++sweep) {
             if (tid == 0) rot_any = 0;
             __syncthreads();
             for (int r = 0; r < S - 1; ++r) {
@@ -366,7 +491,11 @@ cudaError_t launch_ttsvd_big(const TtsvdArgs& a, void* workspace, cudaStream_t s
     int dev = 0, sms = 0, occ = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttsvd_big_kernel, kBigThreads, 0)) != cudaSuccess)
+    if ((e = cudaFuncSetAttribute(ttsvd_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynBytes)) !=
+        cudaSuccess)
+        return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttsvd_big_kernel, kBigThreads, kDynBytes)) !=
+        cudaSuccess)
         return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const int slots = sms * occ;
@@ -378,9 +507,10 @@ cudaError_t launch_ttsvd_big(const TtsvdArgs& a, void* workspace, cudaStream_t s
         const int groups = std::min(per_launch, a.B - b0);
         TtsvdArgs aa = a;
         int64_t wp = per;
-        int Cc = C, bb = b0;
-        void* args[] = {&aa, &ws, &sync, &wp, &Cc, &bb};
-        e = cudaLaunchCooperativeKernel((const void*)ttsvd_big_kernel, dim3(groups * C), dim3(kBigThreads), args, 0, s);
+        int Cc = C, bb = b0, dd = kDynBytes / 8;
+        void* args[] = {&aa, &ws, &sync, &wp, &Cc, &bb, &dd};
+        e = cudaLaunchCooperativeKernel((const void*)ttsvd_big_kernel, dim3(groups * C), dim3(kBigThreads), args,
+                                        kDynBytes, s);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
