@@ -6,7 +6,8 @@ nvidia-smi --query-gpu=name,clocks.max.sm,clocks.max.mem,power.limit --format=cs
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench rc=$?"
-for c in S1 R1 A2; do
+timeout 900 python bench.py --example2 > $O/example2.json 2> $O/example2.err
+for c in S1 R1 A2 A2ii; do
   timeout 600 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/ref_default.json 2> $O/ref_default.err
