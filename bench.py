@@ -211,7 +211,8 @@ def cpu_oracle_rate(cfg: str, X, Y, target_s: float, nthreads: int = None, one_t
         reps += 1
     cb = {"value": reps * count / t, "unit": UNIT, "cores": nthreads, "kind": "oracle", "cpu_model": cpu_model(),
           "sample": f"{reps} pass(es) over the first {count} of {nb} {cfg} pairs (fp64 oracle {_oracle_name(cfg)}, "
-                    f"OpenMP over pairs), {t:.1f} s"}
+                    + ("numpy, pairs one after another" if ttgen.CONFIGS[cfg]["op"] == "alg2" else "OpenMP over pairs")
+                    + f"), {t:.1f} s"}
     if one_thread_s > 0:
         c1 = max(1, min(count, int(count * one_thread_s / max(t / reps * nthreads, 1e-6))))
         t1 = run(c1, 1)
