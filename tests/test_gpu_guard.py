@@ -89,3 +89,64 @@ def test_contract_splice_reconstruct_stay_in_bounds(op):
     assert np.all(np.isfinite(got)), f"{op}: read outside the trains"
     assert np.all(np.isnan(f[:32])) and np.all(np.isnan(f[32 + n:])), f"{op}: wrote outside its output"
     assert np.array_equal(got.view(np.uint32), ref.cpu().numpy().view(np.uint32))
+
+
+def _guarded_ws(nbytes):
+    """(full buffer, the workspace view): 4 KB of 0xFF guard bytes before and after the caller's workspace."""
+    full = torch.full((nbytes + 8192,), 255, dtype=torch.uint8, device=DEV)
+    return full, full[4096: 4096 + nbytes]
+
+
+def test_reconstruct_beyond_shared_memory_stays_in_bounds():
+    """The workspace GEMM chain (reconstruct_big.cu): trains between NaN guard bands, output between NaN sentinels,
+    workspace between guard bytes; result bitwise equal to the plain call."""
+    r = np.tile(np.array([1, 7, 9, 1], np.int32), (3, 1))
+    r[1, 1:-1] = [6, 8]
+    T = ttgen.gaussian_batch(5, 0, 0, 0, r, (7, 2000, 9), "geo")
+    ref = ttc.ttc_reconstruct(ttc.TTDevice.from_batch(T, DEV), [2, 3, 1])
+    TG, _bt = _guarded_copy(T, True)
+    nb = ttc.ttc_reconstruct_workspace(TG, [2, 3, 1])
+    assert nb > 0
+    wfull, ws = _guarded_ws(nb)
+    full, out = _sentinel_out(ref.numel())
+    ttc.ttc_reconstruct(TG, [2, 3, 1], out=out, workspace=ws)
+    torch.cuda.synchronize()
+    got, f, w = out.cpu().numpy(), full.cpu().numpy(), wfull.cpu().numpy()
+    n = got.size
+    assert np.all(np.isfinite(got)), "read outside the trains"
+    assert np.all(np.isnan(f[:32])) and np.all(np.isnan(f[32 + n:])), "wrote outside the output"
+    assert np.all(w[:4096] == 255) and np.all(w[4096 + nb:] == 255), "wrote outside the workspace"
+    assert np.array_equal(got.view(np.uint32), ref.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("dims,perm", [((20, 20, 20, 5), None), ((5, 20, 20, 20), [2, 3, 4, 1]), ((70, 70), None)])
+def test_tt_svd_beyond_shared_memory_stays_in_bounds(dims, perm):
+    """The workspace TT-SVD (ttsvd_big.cu): dense batch between NaN guards, cores / ranks between sentinels, the
+    workspace between guard bytes; cores and ranks bitwise equal to the plain call."""
+    B = 3
+    n = int(np.prod(dims))
+    rng = np.random.default_rng(n)
+    dense = torch.from_numpy(rng.standard_normal(B * n).astype(np.float32)).to(DEV)
+    ref = ttc.ttc_tt_svd(dense, dims, 0.1, perm=perm)
+    cap = ttc.ttc_tt_svd_capacity(dims, perm)
+    dfull = torch.full((B * n + 2 * GUARD,), float("nan"), dtype=torch.float32, device=DEV)
+    dfull[GUARD: GUARD + B * n] = dense
+    cfull, cores = _sentinel_out(B * cap)
+    rfull = torch.full((B * (len(dims) + 1) + 64,), -7, dtype=torch.int32, device=DEV)
+    ranks = rfull[32: 32 + B * (len(dims) + 1)].view(B, len(dims) + 1)
+    nb = ttc.ttc_tt_svd_workspace(B, dims, perm)
+    wfull, ws = _guarded_ws(nb)
+    ttc.ttc_tt_svd_into(dfull[GUARD: GUARD + B * n], dims, 0.1, cores, ranks, perm=perm, workspace=ws)
+    torch.cuda.synchronize()
+    rk = ranks.cpu().numpy()
+    assert np.array_equal(rk, ref.rank_rows()), "ranks differ from the plain call"
+    c, cf, rf, w = cores.cpu().numpy(), cfull.cpu().numpy(), rfull.cpu().numpy(), wfull.cpu().numpy()
+    assert np.all(np.isnan(cf[:32])) and np.all(np.isnan(cf[32 + B * cap:])), "wrote outside the cores"
+    assert np.all(rf[:32] == -7) and np.all(rf[32 + B * (len(dims) + 1):] == -7), "wrote outside the ranks"
+    assert np.all(w[:4096] == 255) and np.all(w[4096 + nb:] == 255), "wrote outside the workspace"
+    refc = ref.cores.cpu().numpy()
+    for b in range(B):   # the written part of each train: finite (no read outside the dense batch) and bitwise equal
+        used = sum(int(rk[b][k]) * (ref.dims_np[k]) * int(rk[b][k + 1]) for k in range(len(dims)))
+        seg = c[b * cap: b * cap + used]
+        assert np.all(np.isfinite(seg)), "read outside the dense batch"
+        assert np.array_equal(seg.view(np.uint32), refc[b * cap: b * cap + used].view(np.uint32))

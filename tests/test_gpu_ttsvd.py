@@ -239,3 +239,38 @@ def test_example2_alg2_on_gpu(case):
         got = dense[b * n_el:(b + 1) * n_el].reshape(want.shape, order="F")
         err = np.linalg.norm(got - want) / (np.linalg.norm(Xs[b]) * np.linalg.norm(Ys[b]))
         assert err <= 1e-5, f"pair {b}: {err:.3e}"
+
+
+def test_big_path_in_chunks_matches_fused_kernel(monkeypatch):
+    """More tensors than co-resident CTAs (200 > 148): the workspace kernel runs in several cooperative launches
+    of whole groups; ranks and cores equal the fused shared-memory kernel's to fp32 rounding."""
+    dims, B = (12, 10, 9), 200
+    rng = np.random.default_rng(77)
+    Xs = [rng.standard_normal(dims) for _ in range(B)]
+    dense = _dense_batch(Xs)
+    monkeypatch.setenv("TTC_TTSVD_FUSED", "1")
+    T_f = ttc.ttc_tt_svd(dense, dims, 0.05)
+    monkeypatch.delenv("TTC_TTSVD_FUSED")
+    monkeypatch.setenv("TTC_TTSVD_BIG", "1")
+    T_b = ttc.ttc_tt_svd(dense, dims, 0.05)
+    monkeypatch.delenv("TTC_TTSVD_BIG")
+    assert np.array_equal(T_f.rank_rows(), T_b.rank_rows())
+    for b, (cf, cb) in enumerate(zip(_trains(T_f), _trains(T_b))):
+        scale = np.linalg.norm(Xs[b])
+        for f, g in zip(cf, cb):
+            assert np.max(np.abs(f - g)) <= 1e-4 * max(1.0, scale), f"tensor {b}: cores differ"
+
+
+def test_example2_permuted_big_operand():
+    """Alg. 2 step 1's permutation folded into the workspace kernel's read: the TT of X^rho (X of shape
+    5 x 20 x 20 x 20, rho = (2, 3, 4, 1): 20 x 20 x 20 x 5) equals O6's TT-SVD of numpy's transpose."""
+    rng = np.random.default_rng(21)
+    dims, perm = (5, 20, 20, 20), [2, 3, 4, 1]
+    Xs = [rng.standard_normal(dims).astype(np.float32).astype(np.float64) for _ in range(2)]
+    T = ttc.ttc_tt_svd(_dense_batch(Xs), dims, 0.0, perm=perm)
+    for b, cs in enumerate(_trains(T)):
+        Xr = np.transpose(Xs[b], [p - 1 for p in perm])
+        want = ttsvd.tt_svd(Xr, 0.0)
+        assert [c.shape for c in cs] == [w.shape for w in want]
+        for c, w in zip(cs, want):
+            assert np.max(np.abs(c - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))
