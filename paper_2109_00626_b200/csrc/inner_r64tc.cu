@@ -37,7 +37,12 @@ using namespace tc;
 
 constexpr int kTile = 16384;                      // bytes of one staged tile
 constexpr int kRaw = 4, kLo = 3;                  // ring depths (raw input tiles / their lo parts)
-constexpr int kThreads = 256;                   // 8 warps (see the roles below): 2 per SM sub-partition
+#ifndef TTC_R64TC_LO_WARPS
+#define TTC_R64TC_LO_WARPS 2
+#endif
+constexpr int kLoWarps = TTC_R64TC_LO_WARPS;       // lo workers (warps 6 ..); 4 measured 0.94M vs 1.69M pairs/s
+                                                   // (168 registers: the epilogue spills)
+constexpr int kThreads = 32 * (6 + kLoWarps);      // TMA, MMA, 4 epilogue warps, the lo workers
 constexpr int kTilesPerStep = 8;                  // Y halves (2 K-chunks each), then X slices 0..3
 
 // shared-memory layout (bytes from the 1024-aligned base)
@@ -203,7 +208,7 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRaw; ++i) { mbar_init(bar_at(sm, FULL + i), 1); mbar_init(bar_at(sm, EMPTY + i), 1); }
-        for (int i = 0; i < kLo; ++i) { mbar_init(bar_at(sm, LO_READY + i), 2); mbar_init(bar_at(sm, LO_FREE + i), 1); }
+        for (int i = 0; i < kLo; ++i) { mbar_init(bar_at(sm, LO_READY + i), kLoWarps); mbar_init(bar_at(sm, LO_FREE + i), 1); }
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar_at(sm, D2P_FULL + i), 1); mbar_init(bar_at(sm, D2P_EMPTY + i), 4);
             mbar_init(bar_at(sm, D1_FULL + i), 1); mbar_init(bar_at(sm, D1_EMPTY + i), 4);
@@ -338,7 +343,8 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
         // ================================================================ lo workers (warps 6, 7)
         // the lo part of every staged input tile, in the order the MMA issuer consumes them (elementwise: the lo
         // tile has the raw tile's byte layout); all loads of a thread's share are issued before any store
-        const int ct = threadIdx.x - 192;         // 0..63
+        constexpr int kLoT = 32 * kLoWarps;       // lo threads
+        const int ct = threadIdx.x - 192;         // 0 .. kLoT - 1
         uint32_t ktot = 0;
         for (int idx = blockIdx.x; idx < a.B; idx += gridDim.x) ktot += (uint32_t)steps * kTilesPerStep;
         for (uint32_t k = 0; k < ktot; ++k) {
@@ -349,11 +355,11 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
             float4* dst = reinterpret_cast<float4*>(sm + kOffLo + l * kTile);
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-                float4 r[kTile / 16 / 128];
+                float4 r[kTile / 16 / (2 * kLoT)];
 #pragma unroll
-                for (int e = 0; e < kTile / 16 / 128; ++e) r[e] = src[ct + 64 * (2 * e + hf)];
+                for (int e = 0; e < kTile / 16 / (2 * kLoT); ++e) r[e] = src[ct + kLoT * (2 * e + hf)];
 #pragma unroll
-                for (int e = 0; e < kTile / 16 / 128; ++e) dst[ct + 64 * (2 * e + hf)] = lo_rn4(r[e]);
+                for (int e = 0; e < kTile / 16 / (2 * kLoT); ++e) dst[ct + kLoT * (2 * e + hf)] = lo_rn4(r[e]);
             }
             fence_proxy_async();
             __syncwarp();
