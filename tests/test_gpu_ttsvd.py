@@ -274,3 +274,21 @@ def test_example2_permuted_big_operand():
         assert [c.shape for c in cs] == [w.shape for w in want]
         for c, w in zip(cs, want):
             assert np.max(np.abs(c - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))
+
+
+@pytest.mark.parametrize("dims", [(20000,), (1, 20000), (20000, 1), (3, 1, 7000), (130, 130)])
+def test_big_path_degenerate_shapes(dims):
+    """The workspace kernel on its degenerate cases: order 1 (the train is the tensor), unit modes (one-column
+    unfoldings: no rotation), a zero tensor (every rank 1, the train's product zero), against O6."""
+    rng = np.random.default_rng(len(dims))
+    X = rng.standard_normal(dims).astype(np.float32).astype(np.float64)
+    Z0 = np.zeros(dims)
+    T = ttc.ttc_tt_svd(_dense_batch([X, Z0]), dims, 0.0)
+    got = _trains(T)
+    want = ttsvd.tt_svd(X, 0.0)
+    assert [c.shape for c in got[0]] == [w.shape for w in want]
+    for c, w in zip(got[0], want):
+        assert np.max(np.abs(c - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))
+    # zero tensor: every rank 1 (R23 with s_0 = 0), a train whose product is exactly zero
+    assert all(c.shape[0] == 1 and c.shape[2] == 1 for c in got[1])
+    assert np.all(ref.dense_from_tt(got[1]) == 0)
