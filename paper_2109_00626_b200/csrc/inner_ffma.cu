@@ -21,6 +21,7 @@
 // (a "snake" over the cost-descending list of ttc_inner_ordered balances heterogeneous pairs); no global state,
 // so concurrent launches and graph replays on several streams are independent (re-entrant, ttc.h).
 #include <algorithm>
+#include <cstdlib>
 
 #include "tc_common.cuh"
 #include "ttc_internal.h"
@@ -52,6 +53,7 @@ struct FStep {
     int start;        // ring offset (floats) of the F region (boundary steps: X), G (Y) follows
     int b, n, R, P, S, Q, I;
     int vf;           // interior: V-first (F = X); boundary: unused
+    int part;         // interior: 0 the whole step, 1 its F operand only (GEMM-1), 2 its G operand only (GEMM-2)
     int znext;        // orientation the next step wants Z in (1: transposed, V-first next)
     unsigned end;     // monotone ring position after this step
 };
@@ -205,15 +207,18 @@ __device__ __noinline__ void ff_gemm(const float* A, int sA, const float* B, int
 // column c = i + I f' (so that GEMM-2 reads W column f' as one contiguous run over (g, i)); GEMM-2 writes Z'
 // in the orientation the next step reads: same (flip = 0): [g'][f'] stride Fb + kPad; flip: [f'][g'] stride
 // Gb + kPad.
-__device__ __forceinline__ void ff_step(const float* F, int Fa, int Fb, const float* G, int Ga, int Gb, int I, float* Z,
-                                        float* W, int flip, int lane) {
+__device__ __forceinline__ void ff_step1(const float* F, int Fa, int Fb, int Ga, int I, const float* Z, float* W,
+                                         int lane) {
     const unsigned idiv = I == 1 ? 0u : c_magic.v[I];
-    const int sF = Fa + kPad, sG = Ga * I + kPad;
+    const int sF = Fa + kPad;
     // GEMM-1: W[g, c] = sum_f Z[g, f] F[f, c]     (Ga x I Fb, K = Fa)
     ff_gemm(Z, sF, F, sF, Fa, Ga >> 3, (I * Fb) >> 2, W, 1, I == 1 ? Ga + kPad : Ga, I == 1 ? 0 : kPad, idiv, lane);
     __syncwarp();
+}
+__device__ __forceinline__ void ff_step2(int Fb, const float* G, int Ga, int Gb, int I, float* Z, const float* W,
+                                         int flip, int lane) {
+    const int sG = Ga * I + kPad, sW = Ga * I + kPad;
     // GEMM-2: Z'[g', f'] = sum_(g,i) G[(g,i), g'] W[(g,i), f']   (Gb x Fb, K = Ga I)
-    const int sW = Ga * I + kPad;
     ff_gemm(G, sG, W, sW, Ga * I, Gb >> 3, Fb >> 2, Z, flip ? 1 : Fb + kPad, flip ? Gb + kPad : 1, 0, 0u, lane);
     __syncwarp();
 }
@@ -250,6 +255,7 @@ struct FCursor {
     int b, n, R, P;
     int64_t xo, yo;
     bool valid;
+    bool half;        // the current step is split and its F part is staged: G next
     unsigned k;       // pairs taken so far by this warp
 };
 
@@ -270,6 +276,7 @@ __device__ __forceinline__ void fc_pop(const InnerArgs& a, const FfArgs&, FCurso
     }
     __syncwarp();
     c.n = 0;
+    c.half = false;
     c.R = 1;
     c.P = 1;
     c.xo = fbase(a.x, c.b);
@@ -299,13 +306,18 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
             const int R = ic.R, P = ic.P;
             const int S = rk[n + 1], Q = rk[N + 2 + n];
             const bool boundary = n == 0 || n == N - 1;
-            int vf = 0, need;
+            int vf = 0, need, part = 0;
             if (boundary) {
                 need = ((R * I * S + 3) & ~3) + ((P * I * Q + 3) & ~3);
             } else {
                 vf = vfirst(R, P, S, Q);
                 const int Fa = vf ? R : P, Fb = vf ? S : Q, Ga = vf ? P : R, Gb = vf ? Q : S;
-                need = I * Fb * (Fa + kPad) + Gb * (Ga * I + kPad);
+                const int needF = I * Fb * (Fa + kPad), needG = Gb * (Ga * I + kPad);
+                need = needF + needG;
+                if ((unsigned)need > RING) {   // a step larger than the ring: its F and G operands one after the other
+                    part = ic.half ? 2 : 1;
+                    need = part == 1 ? needF : needG;
+                }
             }
             unsigned start = head, start_off = head_off;
             if (start_off + need > RING) { start += RING - start_off; start_off = 0; }   // never wrap a step
@@ -321,8 +333,8 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
                 const float* Fs = vf ? xs : ys;
                 const float* Gs = vf ? ys : xs;
                 const int Fa = vf ? R : P, Fb = vf ? S : Q, Ga = vf ? P : R, Gb = vf ? Q : S;
-                stage_padded(dst, Fs, I * Fb, Fa, lane);
-                stage_padded(dst + I * Fb * (Fa + kPad), Gs, Gb, Ga * I, lane);
+                if (part != 2) stage_padded(dst, Fs, I * Fb, Fa, lane);
+                if (part != 1) stage_padded(part == 2 ? dst : dst + I * Fb * (Fa + kPad), Gs, Gb, Ga * I, lane);
             }
             tc::cp_commit_group();
             int znext = 0;   // the next step's Z orientation (the last step reads [r][p])
@@ -332,6 +344,7 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
                 f.start = (int)start_off;
                 f.b = ic.b; f.n = n; f.R = R; f.P = P; f.S = S; f.Q = Q; f.I = I;
                 f.vf = vf;
+                f.part = part;
                 f.znext = znext;
                 f.end = start + need;
                 q[(qh + qn) % kQ] = f;
@@ -339,6 +352,11 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
             ++qn;
             head = start + need;
             head_off = start_off + need;
+            if (part == 1) {   // the same step's G operand is staged next
+                ic.half = true;
+                continue;
+            }
+            ic.half = false;
             ic.xo += (int64_t)R * I * S;
             ic.yo += (int64_t)P * I * Q;
             ic.R = S;
@@ -361,8 +379,14 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
         } else {
             const int vf = f.vf;
             const int Fa = vf ? f.R : f.P, Fb = vf ? f.S : f.Q, Ga = vf ? f.P : f.R, Gb = vf ? f.Q : f.S;
-            const float* G = X + f.I * Fb * (Fa + kPad);
-            ff_step(X, Fa, Fb, G, Ga, Gb, f.I, Z, W, f.znext != vf, lane);
+            if (f.part == 0) {
+                ff_step1(X, Fa, Fb, Ga, f.I, Z, W, lane);
+                ff_step2(Fb, X + f.I * Fb * (Fa + kPad), Ga, Gb, f.I, Z, W, f.znext != vf, lane);
+            } else if (f.part == 1) {
+                ff_step1(X, Fa, Fb, Ga, f.I, Z, W, lane);
+            } else {
+                ff_step2(Fb, X, Ga, Gb, f.I, Z, W, f.znext != vf, lane);
+            }
         }
         __syncwarp();
         tail = f.end;
@@ -374,12 +398,13 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
 
 // Floats of the per-warp buffers for a batch whose interior ranks are <= max_rank and dims <= max_dim.
 struct FfSizes {
-    int64_t step, zbuf, wbuf, qf;   // qf: step queue + the staged pair's rank rows
+    int64_t step, half, zbuf, wbuf, qf;   // qf: step queue + the staged pair's rank rows
 };
 FfSizes ffma_sizes(int max_rank, int max_dim, int N) {
     const int64_t r = max_rank, I = max_dim;
     FfSizes z;
     z.step = I * r * (r + kPad) + r * (r * I + kPad) + 64;   // padded F + G regions of the largest step (+ slack)
+    z.half = std::max(I * r * (r + kPad), r * (r * I + kPad)) + 64;   // its larger operand (a split step)
     z.zbuf = r * (r + kPad);
     z.wbuf = r * (r * I + kPad);
     z.qf = (kQ * (int64_t)sizeof(FStep) / 4 + 2 * (N + 1) + 3) & ~int64_t(3);
@@ -396,7 +421,7 @@ bool inner_ffma_supported(const InnerArgs& a, int max_rank, bool ranks_mult8) {
     if (max_rank * max_dim / 4 > kMagicMax) return false;
     const FfSizes z = ffma_sizes(max_rank, max_dim, a.N);
     // at least 4 warps per SM, each holding one step of the largest shape
-    return 4 * (4 * (z.step + z.zbuf + z.wbuf + z.qf) + kReservedPerCTA) <= kSmemPerSM;
+    return 4 * (4 * (z.step + z.zbuf + z.wbuf + z.qf) + kReservedPerCTA) <= kSmemPerSM;   // (z.half: split steps)
 }
 
 cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s) {
@@ -408,7 +433,12 @@ cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s) 
     // (shared memory is allocated per CTA in 256-byte units, plus 1 KB reserved per CTA)
     auto cta_bytes = [](int64_t floats) { return ((4 * floats + 255) & ~int64_t(255)) + kReservedPerCTA; };
     int per_sm = 16;
-    while (per_sm > 1 && per_sm * cta_bytes(z.step + fixed) > kSmemPerSM) --per_sm;
+    // Steps larger than the ring are staged in two parts (F, then G), so the ring needs only the largest operand;
+    // but a split step exposes a DRAM round trip, so the ring keeps at least 3/4 of the largest step (C5: 8 warps
+    // per SM with rank-32 steps split, measured +8% over 7 warps holding whole steps; 9 warps: -5%)
+    const int64_t ring_min = std::max(z.half, (3 * z.step) / 4);
+    while (per_sm > 1 && per_sm * cta_bytes(ring_min + fixed) > kSmemPerSM) --per_sm;
+    if (const char* v = std::getenv("TTC_FFMA_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(v)));
     int64_t warp_floats = (((kSmemPerSM / per_sm - kReservedPerCTA) & ~int64_t(255)) / 4);
     warp_floats = std::min<int64_t>(warp_floats, kSmemPerCTA / 4);
     FfArgs w;
