@@ -30,7 +30,10 @@ namespace ttc {
 namespace {
 
 constexpr int kPad = 4;
-constexpr int kQ = 4;                   // staged steps in flight per warp
+#ifndef TTC_FFMA_Q
+#define TTC_FFMA_Q 4
+#endif
+constexpr int kQ = TTC_FFMA_Q;          // staged steps in flight per warp (queue entries)
 
 constexpr int kMagicMax = 1024;          // exact-division table: q in [2, kMagicMax]
 
