@@ -296,8 +296,22 @@ def make_work(ttc, cfg, b0, B, seed, dev, stream, ranks=None):
         Nd = len(shape)
         px = [c["x_mode"]] + [k for k in range(1, Nd + 1) if k != c["x_mode"]]
         py = [c["y_mode"]] + [k for k in range(1, Nd + 1) if k != c["y_mode"]]
-        TX = ttc.ttc_tt_svd(X, shape, c["eps"], perm=px)
-        TY = ttc.ttc_tt_svd(Y, shape, c["eps"], perm=py)
+        n_in = int(np.prod(shape))
+        joint = px == py   # same shape and permutation: one TT-SVD launch sequence over the 2B tensors [X; Y]
+        if joint:
+            XY = torch.empty(2 * B * n_in, dtype=torch.float32, device=dev)
+            XY[:B * n_in].copy_(X)
+            XY[B * n_in:].copy_(Y)
+            X, Y = XY[:B * n_in], XY[B * n_in:]   # the e2e leg copies the host inputs into these views
+            TXY = ttc.ttc_tt_svd(XY, shape, c["eps"], perm=px)
+            cap = ttc.ttc_tt_svd_capacity(shape, px)
+            rows = TXY.rank_rows()
+            offs = np.arange(B, dtype=np.int64) * cap
+            TX = ttc.TTDevice(TXY.cores[:B * cap], TXY.dims_np, ranks=rows[:B], offsets=offs)
+            TY = ttc.TTDevice(TXY.cores[B * cap:], TXY.dims_np, ranks=rows[B:], offsets=offs)
+        else:
+            TX = ttc.ttc_tt_svd(X, shape, c["eps"], perm=px)
+            TY = ttc.ttc_tt_svd(Y, shape, c["eps"], perm=py)
         plan = ttc.ttc_splice_plan_create(TX, TY, 1, 1)
         rx_dev = torch.from_numpy(TX.rank_rows()).to(dev)
         ry_dev = torch.from_numpy(TY.rank_rows()).to(dev)
@@ -306,11 +320,13 @@ def make_work(ttc, cfg, b0, B, seed, dev, stream, ranks=None):
         n_out = int(np.prod(plan.dims.astype(np.int64)))
         out = torch.empty(B * n_out, dtype=torch.float32, device=dev)
         rk_x, rk_y = torch.empty_like(rx_dev), torch.empty_like(ry_dev)
-        ws_x = torch.empty(max(16, ttc.ttc_tt_svd_workspace(B, shape, px)), dtype=torch.uint8, device=dev)
-        ws_y = torch.empty(max(16, ttc.ttc_tt_svd_workspace(B, shape, py)), dtype=torch.uint8, device=dev)
+        ws_x = torch.empty(max(16, ttc.ttc_tt_svd_workspace(2 * B if joint else B, shape, px)), dtype=torch.uint8,
+                           device=dev)
+        ws_y = None if joint else torch.empty(max(16, ttc.ttc_tt_svd_workspace(B, shape, py)), dtype=torch.uint8,
+                                              device=dev)
+        rk_xy = torch.empty((2 * B, len(shape) + 1), dtype=torch.int32, device=dev) if joint else None
         nb_r = ttc.ttc_reconstruct_workspace(ZD, plan.perm)
         ws_r = torch.empty(nb_r, dtype=torch.uint8, device=dev) if nb_r else None
-        n_in = int(np.prod(shape))
         train_x = int(sum(int(a) * int(i) * int(b2) for a, i, b2 in
                           zip(TX.rank_rows()[0][:-1], TX.dims_np, TX.rank_rows()[0][1:])))
         w.alg_bytes = 4.0 * B * (2 * n_in + 2 * 2 * train_x + 2 * (plan.total // B) + n_out)
@@ -322,6 +338,9 @@ def make_work(ttc, cfg, b0, B, seed, dev, stream, ranks=None):
             w.alg_flops = 0.0
 
         def svd():
+            if joint:
+                ttc.ttc_tt_svd_into(XY, shape, c["eps"], TXY.cores, rk_xy, perm=px, stream=stream, workspace=ws_x)
+                return
             ttc.ttc_tt_svd_into(X, shape, c["eps"], TX.cores, rk_x, perm=px, stream=stream, workspace=ws_x)
             ttc.ttc_tt_svd_into(Y, shape, c["eps"], TY.cores, rk_y, perm=py, stream=stream, workspace=ws_y)
 
@@ -341,7 +360,7 @@ def make_work(ttc, cfg, b0, B, seed, dev, stream, ranks=None):
         # the reconstruction 1 launch (shared memory) or L - 1 (workspace GEMM chain, L = output order)
         side = max(min(int(np.prod(shape[:n + 1])), int(np.prod(shape[n + 1:]))) for n in range(Nd - 1))
         per_svd = 1 + 2 * (Nd - 1) if side <= 32 else 1
-        w.launches = 2 * per_svd + 1 + (len(plan.dims) - 1 if nb_r else 1)
+        w.launches = (1 if joint else 2) * per_svd + 1 + (len(plan.dims) - 1 if nb_r else 1)
         w.plan, w.TX = plan, TX
     elif c["op"] == "reconstruct":
         n_el = c["I"] ** c["N"]
