@@ -159,18 +159,20 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
         // ---- one-sided Jacobi sweeps
         const int S = s + (s & 1);
         const bool cta_pairs = L >= kCtaPairL;
-        int bs = 16;   // block mode: columns per block (two blocks and their rotation matrix in shared memory)
-        while (bs > 4 && (int64_t)L * 2 * bs + 4 * bs * bs > dyn_doubles) bs >>= 1;
-        const bool block_mode = !cta_pairs && s >= 32 && (int64_t)L * 2 * bs + 4 * bs * bs <= dyn_doubles;
+        // block mode: columns per block (two blocks of A and their rotation matrix Q -- always 32 x 32, identity
+        // past the pair's columns, so the V update can run its fixed 32-term loop -- in shared memory)
+        int bs = 16;
+        while (bs > 4 && (int64_t)L * 2 * bs + kMaxBlk2 * kMaxBlk2 > dyn_doubles) bs >>= 1;
+        const bool block_mode = !cta_pairs && s >= 32 && (int64_t)L * 2 * bs + kMaxBlk2 * kMaxBlk2 <= dyn_doubles;
         if (block_mode) {
             // Block one-sided Jacobi: the s columns in nb blocks of bs, block pairs in the round-robin order (one
             // CTA per block pair, nb - 1 group barriers per sweep instead of s - 1); a block pair is loaded into
             // shared memory and orthogonalised there by local round-robin sweeps (warp per column pair), its
             // rotations accumulated in a 2bs x 2bs matrix Q and applied to V's columns once: V_pair <- V_pair Q.
             const int nb0 = (s + bs - 1) / bs, nb = nb0 + (nb0 & 1);
-            const int ldq = 2 * bs;
+            const int ldq = kMaxBlk2;
             double* As = dsm;                             // nl columns of L doubles
-            double* Qm = dsm + (int64_t)L * 2 * bs;       // nl x nl, column-major, leading dimension 2 bs
+            double* Qm = dsm + (int64_t)L * 2 * bs;       // 32 x 32, column-major (the pair's nl x nl in the corner)
             for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
                 if (tid == 0) rot_any = 0;
                 __syncthreads();

@@ -292,3 +292,15 @@ def test_big_path_degenerate_shapes(dims):
     # zero tensor: every rank 1 (R23 with s_0 = 0), a train whose product is exactly zero
     assert all(c.shape[0] == 1 and c.shape[2] == 1 for c in got[1])
     assert np.all(ref.dense_from_tt(got[1]) == 0)
+
+
+@pytest.mark.parametrize("dims", [(900, 40), (40, 900), (1000, 300)])
+def test_big_path_narrow_blocks(dims):
+    """Long columns (L > 768) put the block one-sided Jacobi on 8- or 4-column blocks; cores against O6."""
+    rng = np.random.default_rng(sum(dims))
+    X = rng.standard_normal(dims).astype(np.float32).astype(np.float64)
+    T = ttc.ttc_tt_svd(_dense_batch([X]), dims, 0.0)
+    got, want = _trains(T)[0], ttsvd.tt_svd(X, 0.0)
+    assert [c.shape for c in got] == [w.shape for w in want]
+    for c, w in zip(got, want):
+        assert np.max(np.abs(c - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))
