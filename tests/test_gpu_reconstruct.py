@@ -155,3 +155,29 @@ def test_output_stride_one_mode_placement(N, perm_first):
     rest = [k for k in range(1, N + 1) if k != perm_first]
     perm = [perm_first] + list(rng.permutation(rest))
     _check(T, _recon(T, perm), perm)
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_out_offsets(big, monkeypatch):
+    """Caller-given output offsets (out_offsets_dev: trains in reverse order with gaps): every train's dense tensor
+    lands at its offset, bitwise equal to the packed call, and nothing is written in the gaps."""
+    if big:
+        monkeypatch.setenv("TTC_RECON_BIG", "1")
+    rng = np.random.default_rng(8)
+    dims, B = (5, 4, 3, 6), 4
+    r = np.stack([[1] + list(rng.integers(1, 6, 3)) + [1] for _ in range(B)]).astype(np.int32)
+    T = ttgen.gaussian_batch(3, 0, 0, 0, r, dims, "geo")
+    TD = ttc.TTDevice.from_batch(T, DEV)
+    packed = ttc.ttc_reconstruct(TD, [2, 1, 4, 3]).cpu().numpy()
+    n_el = int(np.prod(dims))
+    gap = 37
+    offs = np.array([(B - 1 - b) * (n_el + gap) + gap for b in range(B)], np.int64)
+    out = torch.full((B * (n_el + gap) + gap,), float("nan"), dtype=torch.float32, device=DEV)
+    ttc.ttc_reconstruct(TD, [2, 1, 4, 3], out=out, out_offsets=torch.from_numpy(offs).to(DEV))
+    got = out.cpu().numpy()
+    written = np.zeros(got.size, bool)
+    for b in range(B):
+        seg = got[offs[b]: offs[b] + n_el]
+        assert np.array_equal(seg.view(np.uint32), packed[b * n_el:(b + 1) * n_el].view(np.uint32)), f"train {b}"
+        written[offs[b]: offs[b] + n_el] = True
+    assert np.all(np.isnan(got[~written])), "wrote into a gap"
