@@ -196,6 +196,72 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                         const bool full = r == 0;
                         const int S2 = nl + (nl & 1), M = max(np, nq);
                         const int nrl = full ? S2 - 1 : M;
+                        if (!full && L <= 32 * kRegCol) {
+                            // cross rounds with short columns: warp w keeps its P column (local w) in registers for
+                            // all M rounds and only streams the partner Q columns through shared memory
+                            if (tid == 0) lrot = 0;
+                            __syncthreads();
+                            double xr[kRegCol];
+                            double* xcol = As + (int64_t)L * warp;
+                            if (warp < np) {
+#pragma unroll
+                                for (int t = 0; t < kRegCol; ++t) {
+                                    const int e = lane + 32 * t;
+                                    xr[t] = e < L ? xcol[e] : 0.0;
+                                }
+                            }
+                            for (int rl = 0; rl < nrl; ++rl) {
+                                if (warp < np) {
+                                    const int jq = (warp + rl) % M;
+                                    if (jq < nq) {
+                                        const int qa = np + jq;
+                                        double* y = As + (int64_t)L * qa;
+                                        double yr[kRegCol];
+                                        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+                                        for (int t = 0; t < kRegCol; ++t) {
+                                            const int e = lane + 32 * t;
+                                            yr[t] = e < L ? y[e] : 0.0;
+                                        }
+#pragma unroll
+                                        for (int t = 0; t < kRegCol; ++t) {
+                                            al = fma(xr[t], xr[t], al);
+                                            be = fma(yr[t], yr[t], be);
+                                            ga = fma(xr[t], yr[t], ga);
+                                        }
+                                        al = warp_sum(al);
+                                        be = warp_sum(be);
+                                        ga = warp_sum(ga);
+                                        double cs, sn;
+                                        if (rotation(al, be, ga, cs, sn)) {
+#pragma unroll
+                                            for (int t = 0; t < kRegCol; ++t) {
+                                                const int e = lane + 32 * t;
+                                                const double xv = xr[t], yv = yr[t];
+                                                xr[t] = cs * xv - sn * yv;
+                                                if (e < L) y[e] = sn * xv + cs * yv;
+                                            }
+                                            if (lane < nl) {
+                                                const double xv = Qm[lane + ldq * warp], yv = Qm[lane + ldq * qa];
+                                                Qm[lane + ldq * warp] = cs * xv - sn * yv;
+                                                Qm[lane + ldq * qa] = sn * xv + cs * yv;
+                                            }
+                                            if (lane == 0) lrot = 1;
+                                        }
+                                    }
+                                }
+                                __syncthreads();
+                            }
+                            if (warp < np) {
+#pragma unroll
+                                for (int t = 0; t < kRegCol; ++t) {
+                                    const int e = lane + 32 * t;
+                                    if (e < L) xcol[e] = xr[t];
+                                }
+                            }
+                            if (tid == 0 && lrot) lrot_any = 1;
+                            __syncthreads();
+                        } else
                         for (int ls = 0; ls < (full ? kLocalSweeps : 1); ++ls) {
                             if (tid == 0) lrot = 0;
                             __syncthreads();
