@@ -9,7 +9,7 @@
 //            (A V)^T = U^T Z = S V'^T, the next unfolding, directly.
 //   m >  c:  A = Z   (m x c).  Z V = U S  =>  U = columns of Z V / sigma, next unfolding S V^T.
 // Rotations of column pairs in the parallel round-robin order, until a sweep rotates nothing
-// (|a_p . a_q| <= 1e-15 sqrt(|a_p|^2 |a_q|^2)); singular values = norms of A V's columns.  The delta-truncated
+// (|a_p . a_q| <= max(1e-15, sqrt(L) eps) sqrt(|a_p|^2 |a_q|^2)); singular values = norms of A V's columns.  The delta-truncated
 // rank, the 1e-7 singular-value floor (R25) and the sign convention (R24: the largest-magnitude entry of every
 // left singular vector positive, the matching row of S V^T flipped with it) are Alg. 1's as the oracle reads
 // them (oracle/ttsvd.py).  Alg. 2 step 1's permutation is folded into the first read.
@@ -20,6 +20,7 @@
 // 8,000-long columns of case (iii)'s first unfolding).  Every reduction is in a fixed order, so the result does
 // not depend on C.  A, V and Z live in L2 / HBM (a 400 x 400 fp64 A is 1.25 MB).
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 
 #include "ttc_internal.h"
@@ -68,8 +69,8 @@ __device__ __forceinline__ void group_barrier(int* cnt, unsigned& target, int C)
 __device__ __forceinline__ int rr_player(int pos, int r, int S) { return pos == 0 ? 0 : ((pos - 1 + r) % (S - 1)) + 1; }
 
 // Jacobi rotation of columns (ap, aq) given their Gram entries; false when already orthogonal
-__device__ __forceinline__ bool rotation(double al, double be, double ga, double& cs, double& sn) {
-    if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) return false;
+__device__ __forceinline__ bool rotation(double al, double be, double ga, double tol, double& cs, double& sn) {
+    if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) return false;
     const double zeta = (be - al) / (2.0 * ga);
     const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
     cs = 1.0 / sqrt(1.0 + t * t);
@@ -159,6 +160,9 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
         // ---- one-sided Jacobi sweeps
         const int S = s + (s & 1);
         const bool cta_pairs = L >= kCtaPairL;
+        // orthogonality tolerance: the rounding noise of a length-L fp64 dot product (LAPACK dgesvj's sqrt(m) eps);
+        // a fixed 1e-15 kept rotating on that noise for extra sweeps once L grows past ~100
+        const double tol = fmax(1e-15, sqrt((double)L) * DBL_EPSILON);
         // block mode: columns per block (two blocks of A and their rotation matrix Q -- always 32 x 32, identity
         // past the pair's columns, so the V update can run its fixed 32-term loop -- in shared memory)
         int bs = 16;
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                                         be = warp_sum(be);
                                         ga = warp_sum(ga);
                                         double cs, sn;
-                                        if (rotation(al, be, ga, cs, sn)) {
+                                        if (rotation(al, be, ga, tol, cs, sn)) {
 #pragma unroll
                                             for (int t = 0; t < kRegCol; ++t) {
                                                 const int e = lane + 32 * t;
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                                         be = warp_sum(be);
                                         ga = warp_sum(ga);
                                         double cs, sn;
-                                        if (rotation(al, be, ga, cs, sn)) {
+                                        if (rotation(al, be, ga, tol, cs, sn)) {
                                             for (int e = lane; e < L; e += 32) {
                                                 const double xv = x[e], yv = y[e];
                                                 x[e] = cs * xv - sn * yv;
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                         for (int w = 0; w < kBigWarps; ++w) { al += red[0][w]; be += red[1][w]; ga += red[2][w]; }
                         __syncthreads();   // red is reused by the next pair
                         double cs, sn;
-                        if (!rotation(al, be, ga, cs, sn)) continue;   // uniform over the CTA
+                        if (!rotation(al, be, ga, tol, cs, sn)) continue;   // uniform over the CTA
                         for (int e = tid; e < L; e += kBigThreads) {
                             const double x = ap[e], y = aq[e];
                             ap[e] = cs * x - sn * y;
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                             al = warp_sum(al);
                             be = warp_sum(be);
                             ga = warp_sum(ga);
-                            if (!rotation(al, be, ga, cs, sn)) continue;
+                            if (!rotation(al, be, ga, tol, cs, sn)) continue;
 #pragma unroll
                             for (int t = 0; t < kRegCol; ++t) {
                                 const int e = lane + 32 * t;
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(kBigThreads) ttsvd_big_kernel(const TtsvdArgs 
                             al = warp_sum(al);
                             be = warp_sum(be);
                             ga = warp_sum(ga);
-                            if (!rotation(al, be, ga, cs, sn)) continue;
+                            if (!rotation(al, be, ga, tol, cs, sn)) continue;
                             for (int e = lane; e < L; e += 32) {
                                 const double x = ap[e], y = aq[e];
                                 ap[e] = cs * x - sn * y;
