@@ -64,15 +64,26 @@ __host__ __device__ __forceinline__ int ps_y(int floats) {
     return (ps & 7) ? ps : ps + 4;
 }
 
+// Bulk copy with an L2 evict-first policy: every core byte is read exactly once, so it should not displace
+// anything in L2.
+__device__ __forceinline__ void bulk_g2s_once(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 // Producer: stage interior core n (planes of 16 x I floats at the strides above), X planes then Y planes.
 __device__ __forceinline__ void r16_issue(const float* xs, const float* ys, int I, float* stage, uint64_t* bar,
-                                          const R16Layout& lay) {
+                                          const R16Layout& lay, uint64_t pol) {
     const int lane = threadIdx.x & 31;
     const int plane = 16 * I;
     if (lane == 0) mbar_arrive_expect_tx(bar, 4u * 2 * 16 * plane);
     __syncwarp();
-    if (lane < 16) bulk_g2s(stage + lane * ps_x(plane), xs + (int64_t)lane * plane, 4u * plane, bar);
-    else bulk_g2s(stage + lay.x_floats + (lane - 16) * ps_y(plane), ys + (int64_t)(lane - 16) * plane, 4u * plane, bar);
+    if (lane < 16) bulk_g2s_once(stage + lane * ps_x(plane), xs + (int64_t)lane * plane, 4u * plane, bar, pol);
+    else bulk_g2s_once(stage + lay.x_floats + (lane - 16) * ps_y(plane), ys + (int64_t)(lane - 16) * plane, 4u * plane,
+                       bar, pol);
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const float* p) {
@@ -173,6 +184,8 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
     __syncthreads();
 
     if (warp == kCW) {   // ------------------------------------------------------------------ producer warp
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         int j = 0;
         for (int k = 0;; ++k) {
             const R16Pair p = r16_pair(a, k);
@@ -184,7 +197,7 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
                 const int st = j % kStages;
                 if (j >= kStages) mbar_wait(&empty[st], ((j / kStages) - 1) & 1);
                 const int I = a.dims[n];
-                r16_issue(xs + off, ys + off, I, stages + st * lay.stage_floats, &full[st], lay);
+                r16_issue(xs + off, ys + off, I, stages + st * lay.stage_floats, &full[st], lay, pol);
                 off += 256 * (int64_t)I;
             }
         }
