@@ -486,8 +486,8 @@ __device__ __forceinline__ void block_update(const double* __restrict__ G, doubl
 __device__ double* jacobi_pair(double* G, double* Gn, double* V, int n, JacParams& P, int role, int bar) {
     const int lane = threadIdx.x & 31;
     const int np = (n + 1) & ~1, half = np / 2;
-    const int d1 = 32 / half, d2 = 32 - d1 * half;
-    const int k0 = lane / half, q0 = lane - k0 * half;
+    // V is kept TRANSPOSED here (Vt[col][row]: lane = row, so a column rotation is one conflict-free access per
+    // lane); the caller stores it back row-major
     if (role == 1)
         for (int e = lane; e < n * n; e += 32) V[e] = (e / n == e % n) ? 1.0 : 0.0;
     int bp[5];
@@ -545,16 +545,15 @@ __device__ double* jacobi_pair(double* G, double* Gn, double* V, int n, JacParam
             pair_bar(bar);
             const int f = P.ctl[cur];
             if (f & 2) break;
-            if (f & 1) {
-                int k = k0, q = q0;
-                for (int e = lane; e < n * half; e += 32) {      // V J: row k, pair q
-                    if (e != lane) { k += d1; q += d2; if (q >= half) { q -= half; ++k; } }
+            if ((f & 1) && lane < n) {   // V J: lane = row, the round's rotations in turn (broadcast parameters)
+                for (int q = 0; q < half; ++q) {
                     const int x = P.pa[cur][q], y = P.pb[cur][q];
-                    if (y >= n || P.sn[cur][q] == 0.0) continue;
-                    const double c = P.cs[cur][q], sv = P.sn[cur][q];
-                    const double vx = V[k * n + x], vy = V[k * n + y];
-                    V[k * n + x] = c * vx - sv * vy;
-                    V[k * n + y] = sv * vx + c * vy;
+                    const double sv = P.sn[cur][q];
+                    if (y >= n || sv == 0.0) continue;
+                    const double c = P.cs[cur][q];
+                    const double vx = V[x * n + lane], vy = V[y * n + lane];
+                    V[x * n + lane] = c * vx - sv * vy;
+                    V[y * n + lane] = sv * vx + c * vy;
                 }
             }
         }
@@ -590,9 +589,12 @@ __global__ void __launch_bounds__(64 * kJacPairs) ttsvd_jacobi_kernel(const Ttsv
         __syncwarp();
     }
     const double* Gf = jacobi_pair(G, Gn, V, side, P, role, 1 + pair);
-    if (role == 1) {   // V is final: store it
+    if (role == 1) {   // V is final: store it row-major (it was kept transposed)
         double* vdst = w.v + (int64_t)b * g2;
-        for (int e = lane; e < side * side; e += 32) vdst[e] = V[e];
+        for (int e = lane; e < side * side; e += 32) {
+            const int k = e / side, x = e - k * side;
+            vdst[e] = V[x * side + k];
+        }
         return;
     }
     // eigenvalues, descending stable order
