@@ -319,20 +319,28 @@ __device__ void gram_tiled(const float* Z, int m, int ncols, double* g) {
 #pragma unroll
                 for (int v = 0; v < 4; ++v) acc[u][v] = fma(x[u], y[v], acc[u][v]);
         }
+        // butterfly reduce-scatter of the 16 sums over the warp (8 + 4 + 2 + 1 + 1 exchanges instead of 16 x 5):
+        // each level a lane keeps the half of its values selected by one lane bit and adds the partner's copy
+        double r[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int v = 0; v < 4; ++v)
+            for (int v = 0; v < 4; ++v) r[4 * u + v] = acc[u][v];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc[u][v] += __shfl_xor_sync(0xffffffffu, acc[u][v], o);
-        if (l == 0) {
+        for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+            const bool up = (l & o) != 0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int i = i0 + u, j = j0 + v;
-                    if (i < side && j < side) { g[i * side + j] = acc[u][v]; g[j * side + i] = acc[u][v]; }
-                }
+            for (int k = 0; k < h; ++k) {
+                const double send = up ? r[k] : r[k + h];
+                const double keep = up ? r[k + h] : r[k];
+                r[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        r[0] += __shfl_xor_sync(0xffffffffu, r[0], 1);
+        if ((l & 1) == 0) {   // lane 2q holds sum number 8 b4 + 4 b3 + 2 b2 + b1 of its lane bits
+            const int idx = ((l >> 4) & 1) * 8 + ((l >> 3) & 1) * 4 + ((l >> 2) & 1) * 2 + ((l >> 1) & 1);
+            const int i = i0 + (idx >> 2), j = j0 + (idx & 3);
+            if (i < side && j < side) { g[i * side + j] = r[0]; g[j * side + i] = r[0]; }
         }
     }
 }
