@@ -245,10 +245,9 @@ struct StoreD {      // out[offr[row] + offc[col]], m = row, n = col (streaming 
     const int32_t* offr;
     const int32_t* offc;
     int M;
-    __device__ __forceinline__ RowSt row(int m0) const {
-        const int o0 = offr[m0];
-        const bool v4 = m0 + 3 < M && offr[m0 + 1] == o0 + 1 && offr[m0 + 2] == o0 + 2 && offr[m0 + 3] == o0 + 3;
-        return RowSt{m0, o0, v4 ? 1 : 0};
+    __device__ __forceinline__ RowSt row(int m0) const {   // (bit 31 of offr[m0], m0 % 4 == 0: rows m0..m0+3
+        const int o = offr[m0];                                   //  contiguous, set by the kernel's setup pass)
+        return RowSt{m0, o & 0x7fffffff, (int)((unsigned)o >> 31)};
     }
     __device__ __forceinline__ ColSt col(int n) const { return ColSt{out + offc[n], 0}; }
     __device__ __forceinline__ void operator()(const RowSt& rs, const ColSt& c, float4 v) const {
@@ -260,7 +259,7 @@ struct StoreD {      // out[offr[row] + offc[col]], m = row, n = col (streaming 
         const float w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (rs.m0 + u < M) __stcs(c.p + offr[rs.m0 + u], w[u]);
+            if (rs.m0 + u < M) __stcs(c.p + (offr[rs.m0 + u] & 0x7fffffff), w[u]);
     }
 };
 
@@ -306,6 +305,14 @@ __global__ void __launch_bounds__(kThreads, 2) reconstruct_kernel(const ReconArg
         int q = c;
         for (int n = k; n < N; ++n) { const int i = q % a.dims[n]; q /= a.dims[n]; o += (int64_t)i * a.ostride[n]; }
         offc[c] = (int32_t)o;
+    }
+    __syncthreads();
+    // row quads m0 = 4t whose four output rows are consecutive: flagged in bit 31 of offr[m0] (offsets < 2^31), so
+    // the D epilogue decides a 16-byte store with one shared load instead of four
+    for (int t = threadIdx.x; 4 * t + 3 < rows; t += blockDim.x) {
+        const int m0 = 4 * t, o0 = offr[m0];
+        if (offr[m0 + 1] == o0 + 1 && offr[m0 + 2] == o0 + 2 && offr[m0 + 3] == o0 + 3)
+            offr[m0] = (int32_t)((unsigned)o0 | 0x80000000u);
     }
     __syncthreads();
     const int Rk = rk[k];
