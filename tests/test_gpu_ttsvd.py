@@ -304,3 +304,39 @@ def test_big_path_narrow_blocks(dims):
     assert [c.shape for c in got] == [w.shape for w in want]
     for c, w in zip(got, want):
         assert np.max(np.abs(c - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))
+
+
+def test_big_paths_capture_in_a_cuda_graph():
+    """The workspace TT-SVD (cooperative launches + a stream-ordered reset of its barrier counters) and the
+    workspace reconstruction captured in a CUDA graph on a side stream: replays reproduce the direct calls bitwise."""
+    dims, B = (20, 20, 20, 5), 3
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.standard_normal(B * 40000).astype(np.float32)).to(DEV)
+    ref = ttc.ttc_tt_svd(x, dims, 0.0)
+    cap = ttc.ttc_tt_svd_capacity(dims)
+    cores = torch.zeros(B * cap, device=DEV)
+    ranks = torch.zeros((B, len(dims) + 1), dtype=torch.int32, device=DEV)
+    ws = torch.empty(ttc.ttc_tt_svd_workspace(B, dims), dtype=torch.uint8, device=DEV)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ttc.ttc_tt_svd_into(x, dims, 0.0, cores, ranks, workspace=ws)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(cores, ref.cores) and np.array_equal(ranks.cpu().numpy(), ref.rank_rows())
+    # the spliced result of two of them, reconstructed through the workspace path inside a graph
+    plan = ttc.ttc_splice_plan_create(ref, ref, 1, 1)
+    zc, zr, zo = ttc.ttc_contract(plan, ref, ref)
+    Z = ttc.TTDevice(zc, plan.dims, ranks=zr, offsets=zo)
+    want = ttc.ttc_reconstruct(Z, plan.perm)
+    nb = ttc.ttc_reconstruct_workspace(Z, plan.perm)
+    assert nb > 0
+    rws = torch.empty(nb, dtype=torch.uint8, device=DEV)
+    out = torch.empty_like(want)
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2, stream=s):
+        ttc.ttc_reconstruct(Z, plan.perm, out=out, workspace=rws, stream=s)
+    g2.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
