@@ -22,6 +22,7 @@
 // so concurrent launches and graph replays on several streams are independent (re-entrant, ttc.h).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "tc_common.cuh"
 #include "ttc_internal.h"
@@ -50,6 +51,19 @@ struct FfArgs {
     int ring;         // floats of one warp's ring
     int zbuf, wbuf;   // floats of the Z and W buffers
     int warp_floats;  // ring + Z + W + queue
+};
+
+// TMA staging (kTma): one 3-D tensor map per operand buffer and run length L (the contiguous runs an operand is
+// staged in: F runs of Fa floats, G runs of Ga I floats).  Map (L, 8, n / 4) with strides (4 L, 16) bytes and a
+// box of (L + 4, 8, 1): the box starting at coordinate (0, 0, o / 4) is the 8 runs of L floats from float o on,
+// written to shared memory as rows of L + 4 floats -- the padded layout -- with the 4 floats past each run
+// outside the map's first dimension (zero-filled, never read from global memory).  Any 16-byte aligned start is
+// reachable through the third coordinate (runs of 8 rows: every interior F and G operand has a multiple of 8).
+constexpr int kMaxMaps = 16;
+constexpr int kMaxRunQ = 63;      // L / 4 <= 63 (the box's first dimension L + 4 <= 256)
+struct FfMaps {
+    CUtensorMap m[kMaxMaps];
+    unsigned char ix[2][kMaxRunQ + 1];   // [X / Y][L / 4] -> map index
 };
 
 struct FStep {
@@ -287,15 +301,26 @@ __device__ __forceinline__ void fc_pop(const InnerArgs& a, const FfArgs&, FCurso
 }
 
 // One warp per CTA (warps never synchronise with each other); several CTAs per SM, as shared memory allows.
-__global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const FfArgs w) {
-    extern __shared__ __align__(16) float smem[];
+template <bool kTma>
+__global__ void __launch_bounds__(32)
+inner_ffma_kernel(const InnerArgs a, const FfArgs w, const __grid_constant__ FfMaps maps) {
+    extern __shared__ __align__(128) float smem[];
     const int lane = threadIdx.x & 31;
     float* ring = smem;
     float* Z = ring + w.ring;
     float* W = Z + w.zbuf;
     FStep* q = reinterpret_cast<FStep*>(W + w.wbuf);
-    int* rk = reinterpret_cast<int*>(q + kQ);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(q + kQ);   // kTma: one mbarrier per queue entry
+    int* rk = reinterpret_cast<int*>(bars + kQ);
     const int N = a.N;
+    unsigned phase = 0;                                      // kTma: parity bit per queue entry
+    if (kTma) {
+        if (lane == 0) {
+            for (int i = 0; i < kQ; ++i) tc::mbar_init(bars + i, 1);
+            tc::fence_mbar_init();
+        }
+        __syncwarp();
+    }
     FCursor ic;
     ic.k = 0;
     fc_pop(a, w, ic, rk, lane);
@@ -312,6 +337,7 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
             int vf = 0, need, part = 0;
             if (boundary) {
                 need = ((R * I * S + 3) & ~3) + ((P * I * Q + 3) & ~3);
+                if (kTma) need = (need + 31) & ~31;   // every step starts on 128 bytes (TMA destinations)
             } else {
                 vf = vfirst(R, P, S, Q);
                 const int Fa = vf ? R : P, Fb = vf ? S : Q, Ga = vf ? P : R, Gb = vf ? Q : S;
@@ -322,6 +348,8 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
                     need = part == 1 ? needF : needG;
                 }
             }
+            const int tx = need;                      // bytes / 4 the step's TMA boxes deliver (interior)
+            if (kTma) need = (need + 31) & ~31;
             unsigned start = head, start_off = head_off;
             if (start_off + need > RING) { start += RING - start_off; start_off = 0; }   // never wrap a step
             if (qn == 0) tail = start;
@@ -333,11 +361,28 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
                 stage_plain(dst, xs, R * I * S, lane);
                 stage_plain(dst + ((R * I * S + 3) & ~3), ys, P * I * Q, lane);
             } else {
-                const float* Fs = vf ? xs : ys;
-                const float* Gs = vf ? ys : xs;
                 const int Fa = vf ? R : P, Fb = vf ? S : Q, Ga = vf ? P : R, Gb = vf ? Q : S;
-                if (part != 2) stage_padded(dst, Fs, I * Fb, Fa, lane);
-                if (part != 1) stage_padded(part == 2 ? dst : dst + I * Fb * (Fa + kPad), Gs, Gb, Ga * I, lane);
+                if (kTma) {
+                    // F as I Fb / 8 boxes of 8 runs of Fa, G as Gb / 8 boxes of 8 runs of Ga I, one box per lane
+                    uint64_t* bar = bars + (qh + qn) % kQ;
+                    if (lane == 0) tc::mbar_arrive_expect_tx(bar, 4u * (unsigned)tx);
+                    __syncwarp();
+                    const int nf = part != 2 ? (I * Fb) >> 3 : 0, ng = part != 1 ? Gb >> 3 : 0;
+                    for (int j = lane; j < nf + ng; j += 32) {
+                        const bool isF = j < nf;
+                        const int jj = isF ? j : j - nf, L = isF ? Fa : Ga * I;
+                        const bool fromX = isF == (vf != 0);
+                        const int64_t o = (fromX ? ic.xo : ic.yo) + (int64_t)8 * jj * L;
+                        float* d = dst + (isF || part == 2 ? 0 : I * Fb * (Fa + kPad)) + jj * 8 * (L + kPad);
+                        tc::fence_proxy_async();   // the slot's previous (generic-proxy) contents are dead
+                        tc::tma_3d(d, &maps.m[maps.ix[fromX ? 0 : 1][L >> 2]], 0, 0, (int)(o >> 2), bar);
+                    }
+                } else {
+                    const float* Fs = vf ? xs : ys;
+                    const float* Gs = vf ? ys : xs;
+                    if (part != 2) stage_padded(dst, Fs, I * Fb, Fa, lane);
+                    if (part != 1) stage_padded(part == 2 ? dst : dst + I * Fb * (Fa + kPad), Gs, Gb, Ga * I, lane);
+                }
             }
             tc::cp_commit_group();
             int znext = 0;   // the next step's Z orientation (the last step reads [r][p])
@@ -368,9 +413,13 @@ __global__ void __launch_bounds__(32) inner_ffma_kernel(const InnerArgs a, const
         }
         if (qn == 0) break;
         // ---- compute the oldest staged step
-        tc::cp_wait_pending(qn - 1);
+        tc::cp_wait_pending(qn - 1);   // boundary steps (cp.async); kTma: interior steps commit empty groups
         __syncwarp();
         const FStep f = q[qh];
+        if (kTma && f.n != 0 && f.n != N - 1) {
+            tc::mbar_wait(bars + qh, (phase >> qh) & 1u);
+            phase ^= 1u << qh;
+        }
         float* X = ring + f.start;
         if (f.n == N - 1) {   // last step (also N = 1)
             const float* Y = X + ((f.R * f.I * f.S + 3) & ~3);
@@ -410,7 +459,7 @@ FfSizes ffma_sizes(int max_rank, int max_dim, int N) {
     z.half = std::max(I * r * (r + kPad), r * (r * I + kPad)) + 64;   // its larger operand (a split step)
     z.zbuf = r * (r + kPad);
     z.wbuf = r * (r * I + kPad);
-    z.qf = (kQ * (int64_t)sizeof(FStep) / 4 + 2 * (N + 1) + 3) & ~int64_t(3);
+    z.qf = (kQ * (int64_t)sizeof(FStep) / 4 + 2 * kQ + 2 * (N + 1) + 3) & ~int64_t(3);
     return z;
 }
 constexpr int64_t kSmemPerSM = 228 * 1024, kSmemPerCTA = 227 * 1024, kReservedPerCTA = 1024;
@@ -427,11 +476,65 @@ bool inner_ffma_supported(const InnerArgs& a, int max_rank, bool ranks_mult8) {
     return 4 * (4 * (z.step + z.zbuf + z.wbuf + z.qf) + kReservedPerCTA) <= kSmemPerSM;   // (z.half: split steps)
 }
 
-cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s) {
+namespace {
+// The tensor maps of the TMA staging path: every run length an interior step can stage (F: Fa = a rank <= max_rank
+// and a multiple of 8; G: Ga I for the interior dims I), per buffer.  false if a run is too long for one box, the
+// table is full, or an encoding fails -- the launch then stages with cp.async.
+bool ffma_maps(const InnerArgs& a, int max_rank, int64_t nx, int64_t ny, FfMaps* m) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return false;
+    std::memset(m, 0, sizeof(*m));
+    std::memset(m->ix, 0xff, sizeof(m->ix));
+    int runs[kMaxMaps], nr = 0;
+    auto add = [&](int L) {
+        if (L % 4 != 0 || L / 4 > kMaxRunQ) return false;
+        for (int i = 0; i < nr; ++i)
+            if (runs[i] == L) return true;
+        if (2 * (nr + 1) > kMaxMaps) return false;
+        runs[nr++] = L;
+        return true;
+    };
+    for (int r = 8; r <= max_rank; r += 8) {
+        if (!add(r)) return false;
+        for (int n = 1; n + 1 < a.N; ++n)
+            if (!add(r * a.dims[n])) return false;
+    }
+    int k = 0;
+    for (int buf = 0; buf < 2; ++buf) {
+        const float* base = buf ? a.y.cores : a.x.cores;
+        const int64_t n = buf ? ny : nx;
+        if (n / 4 < 1 || n / 4 > (int64_t(1) << 31)) return false;
+        for (int i = 0; i < nr; ++i, ++k) {
+            const int L = runs[i];
+            const cuuint64_t dims[3] = {(cuuint64_t)L, 8, (cuuint64_t)(n / 4)};
+            const cuuint64_t strides[2] = {(cuuint64_t)4 * L, 16};
+            const cuuint32_t box[3] = {(cuuint32_t)L + kPad, 8, 1};
+            const cuuint32_t es[3] = {1, 1, 1};
+            if (enc(&m->m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return false;
+            m->ix[buf][L / 4] = (unsigned char)k;
+        }
+    }
+    return true;
+}
+}  // namespace
+
+cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, bool aligned16, int64_t nx, int64_t ny,
+                              cudaStream_t s) {
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = std::max(max_dim, (int)a.dims[n]);
     const FfSizes z = ffma_sizes(max_rank, max_dim, a.N);
     const int64_t fixed = z.zbuf + z.wbuf + z.qf;
+    // TMA staging unless TTC_FFMA_TMA=0 (A/B) or the maps cannot be built (TTC_FFMA_TMA=1: that is an error)
+    FfMaps maps;          // the kernel parameter (copied at launch)
+    const char* tv = std::getenv("TTC_FFMA_TMA");
+    const bool want_tma = aligned16 && !(tv && tv[0] == '0');
+    const bool tma = want_tma && ffma_maps(a, max_rank, nx, ny, &maps);
+    if (tv && tv[0] == '1' && !tma) return cudaErrorNotSupported;
+    if (!tma) std::memset(maps.ix, 0xff, sizeof(maps.ix));
+    auto kern = tma ? inner_ffma_kernel<true> : inner_ffma_kernel<false>;
     // as many warps per SM as fit with a ring of at least one largest step (at most 16); the ring takes the rest
     // (shared memory is allocated per CTA in 256-byte units, plus 1 KB reserved per CTA)
     auto cta_bytes = [](int64_t floats) { return ((4 * floats + 255) & ~int64_t(255)) + kReservedPerCTA; };
@@ -447,20 +550,20 @@ cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s) 
     FfArgs w;
     w.zbuf = (int)z.zbuf;
     w.wbuf = (int)z.wbuf;
-    w.ring = (int)((warp_floats - fixed) & ~int64_t(3));
+    w.ring = (int)((warp_floats - fixed) & ~int64_t(31));   // 128-byte multiple: TMA destinations stay aligned
     w.warp_floats = (int)(w.ring + fixed);
     const size_t smem = sizeof(float) * (size_t)w.warp_floats;
-    cudaError_t e = cudaFuncSetAttribute(inner_ffma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(inner_ffma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess)
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess)
         return e;
     int dev = 0, sms = 0, occ = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, inner_ffma_kernel, 32, smem)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem)) != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const int grid = std::min(a.B, sms * occ);
-    inner_ffma_kernel<<<grid, 32, smem, s>>>(a, w);
+    kern<<<grid, 32, smem, s>>>(a, w, maps);
     return cudaGetLastError();
 }
 

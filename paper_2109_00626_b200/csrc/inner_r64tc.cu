@@ -127,17 +127,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
-    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                 :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
-    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-                 :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-                 : "memory");
-}
-
 // lo part of a 3xTF32 split: x - trunc_tf32(x) (exact), rounded to nearest tf32 (so the tensor core's own
 // truncation of it is exact and the remaining error has a random sign)
 __device__ __forceinline__ float lo_rn(float x) {
@@ -264,11 +253,11 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                         uint64_t* fb = bar_at(sm, FULL + s);
                         mbar_arrive_expect_tx(fb, kTile);
                         if (t < 4) {   // Y half t/2, K-chunk t%2: box (32 p, 2 i, 64 q)
-                            tma_3d(dst, &tmy, 32 * (t & 1), row, 2 * (t >> 1), fb);
+                            tc::tma_3d(dst, &tmy, 32 * (t & 1), row, 2 * (t >> 1), fb);
                         } else {       // X slice t-4: two boxes (32 r, 64 s)
                             const int i = t - 4;
-                            tma_2d(dst, &tmx, 64 * i, row, fb);
-                            tma_2d(dst + 8192, &tmx, 64 * i + 32, row, fb);
+                            tc::tma_2d(dst, &tmx, 64 * i, row, fb);
+                            tc::tma_2d(dst + 8192, &tmx, 64 * i + 32, row, fb);
                         }
                     }
                 }
@@ -537,11 +526,9 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(kTmemCols));
 }
 
-// ---- host: tensor maps through the driver entry point (no link-time dependency on libcuda)
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+}  // namespace
 
+// ---- host: tensor maps through the driver entry point (no link-time dependency on libcuda)
 EncodeFn encode_fn() {
     static EncodeFn fn = nullptr;
     if (!fn) {
@@ -553,8 +540,6 @@ EncodeFn encode_fn() {
     }
     return fn;
 }
-
-}  // namespace
 
 bool inner_r64tc_supported(const InnerArgs& a, bool uniform_r64) {
     if (!uniform_r64 || a.N < 3 || a.x.offsets || a.y.offsets) return false;

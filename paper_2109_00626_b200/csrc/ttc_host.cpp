@@ -292,9 +292,13 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
             return TTC_OK;
         }
     }
-    const bool ffma_ok = ttc::inner_ffma_supported(a, mr, hx.mult8 && hy.mult8);
+    // every core starts on 16 bytes (the FP32 kernel stages with 16-byte copies): aligned buffers, and offsets
+    // (given, or b * train_elems) multiples of 4 floats
+    const bool cores16 = aligned16 && (x->offsets_host || (hx.train_elems_uniform & 3) == 0) &&
+                         (y->offsets_host || (hy.train_elems_uniform & 3) == 0);
+    const bool ffma_ok = cores16 && ttc::inner_ffma_supported(a, mr, hx.mult8 && hy.mult8);
     if (force_ffma && ffma_ok)
-        e = ttc::launch_inner_ffma(a, mr, s);
+        e = ttc::launch_inner_ffma(a, mr, cores16, x->n_elems, y->n_elems, s);
     else if (!force_generic && !force_fast && ttc::inner_r16_supported(a, uniform_r16))
         e = ttc::launch_inner_r16(a, s);
     else if (!force_generic && !force_mma_sync && ttc::inner_r64tc_supported(a, uniform_r64))
@@ -302,7 +306,7 @@ ttc_status inner_impl(const ttc_tt_batch* x, const ttc_tt_batch* y, const int32_
     else if (!force_generic && ttc::inner_r64_supported(a, uniform_r64))
         e = ttc::launch_inner_r64(a, s);       // legacy mma.sync 3xTF32 (any I_n, offsets allowed)
     else if (!force_generic && !force_fast && ffma_ok)
-        e = ttc::launch_inner_ffma(a, mr, s);   // warp per pair on the FP32 pipe (ranks multiple of 8, <= 32)
+        e = ttc::launch_inner_ffma(a, mr, cores16, x->n_elems, y->n_elems, s);   // warp per pair on the FP32 pipe (ranks multiple of 8, <= 32)
     else if (!force_generic && ttc::inner_fast_supported(a, mr, uniform))
         e = ttc::launch_inner_fast(a, mr, uniform, s);
     else

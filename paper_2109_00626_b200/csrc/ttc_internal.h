@@ -2,6 +2,7 @@
 // Nothing here crosses the C ABI; include/ttc.h is the boundary.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "../../include/ttc.h"
 
@@ -44,7 +45,15 @@ struct SmallLayout {
 };
 cudaError_t launch_inner_small(const InnerArgs& a, const SmallLayout& L, cudaStream_t s);
 bool        inner_ffma_supported(const InnerArgs& a, int max_rank, bool ranks_mult8);
-cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, cudaStream_t s);
+// aligned16: both core buffers 16-byte aligned and every train offset a multiple of 4 floats (the TMA staging
+// path; otherwise 16-byte cp.async); nx / ny: floats at X / Y cores (the tensor maps' extent)
+cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, bool aligned16, int64_t nx, int64_t ny,
+                              cudaStream_t s);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr if unavailable)
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn();
 
 // ---- tt_contract (ladder) ------------------------------------------------------------------------
 enum ElKind : int32_t { EL_XFREE = 1, EL_YFREE = 2, EL_T = 3 };

@@ -358,3 +358,47 @@ def test_graph_replay_and_concurrent_streams_are_reentrant():
         torch.cuda.synchronize()
         for k in range(2):
             assert torch.equal(outs[k], ref[k]), (rep, k)
+
+
+@pytest.mark.parametrize("case", ["c5", "gaps", "dims"])
+def test_ffma_tma_staging_matches_cp_async(monkeypatch, case):
+    """The FP32 kernel's two staging paths (TMA tensor boxes with zero-filled padding, TTC_FFMA_TMA=1, vs 16-byte
+    cp.async, TTC_FFMA_TMA=0) stage the same values, so the results are bitwise equal: C5 correlated pairs; trains
+    at gapped offsets (16-byte steps) with the last core ending at the buffer's end; mixed interior mode sizes
+    (several G run lengths).  Both paths are also checked against the oracle."""
+    rng = np.random.default_rng({"c5": 1, "gaps": 2, "dims": 3}[case])
+    if case == "c5":
+        X, Y = ttgen.config_batch("C5", kind="corr", B=300)
+        XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
+    else:
+        dims = (2,) * 12 if case == "gaps" else (2, 3, 2, 3, 2, 2)   # 8 run lengths: a full map table
+        B, N = 97, len(dims)
+        def ranks():
+            r = rng.choice([8, 16, 24, 32], size=(B, N + 1)).astype(np.int32)
+            r[:, 0] = r[:, -1] = 1
+            return r
+        X = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 0, 0, ranks(), dims, "geo")
+        Y = ttgen.gaussian_batch(int(rng.integers(1 << 30)), 0, 1, 0, ranks(), dims, "geo")
+        def gapped(T):
+            sizes = np.diff(np.append(T.offsets, T.cores.numel()))
+            gaps = 4 * rng.integers(0, 5, size=B)
+            offs = np.zeros(B, np.int64)
+            pos = 0
+            for b in range(B):
+                pos += int(gaps[b])
+                offs[b] = pos
+                pos += int(sizes[b])
+            buf = torch.full((pos,), float("nan"))   # gaps hold NaN: any stray read poisons a result
+            for b in range(B):
+                buf[offs[b]:offs[b] + sizes[b]] = T.cores[T.offsets[b]:T.offsets[b] + sizes[b]]
+            return ttc.TTDevice(buf.to(DEV), T.dims, ranks=T.ranks, offsets=offs)
+        XD, YD = gapped(X), gapped(Y)
+    res = {}
+    for t in ("0", "1"):
+        monkeypatch.setenv("TTC_KERNEL", "ffma")
+        monkeypatch.setenv("TTC_FFMA_TMA", t)
+        res[t] = ttc.ttc_inner(XD, YD).cpu().numpy()
+    monkeypatch.delenv("TTC_FFMA_TMA")
+    monkeypatch.delenv("TTC_KERNEL")
+    assert np.array_equal(res["0"], res["1"])
+    _check(X, Y, res["1"].astype(np.float64), _sample(X.ranks.shape[0], 24, 7), "corr" if case == "c5" else "edge")
