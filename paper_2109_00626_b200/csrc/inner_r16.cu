@@ -22,13 +22,18 @@ namespace {
 
 using namespace tc;
 
-constexpr int kCW = 8;          // compute warps
-constexpr int kCT = 32 * kCW;   // compute threads = zfrag slots (2 x 2 fragments x 64)
-constexpr int kPart = 2 * 32 * 4;   // floats of one warp's partial Z' (2 n-tiles, fragment-native)
-#ifndef TTC_R16_STAGES
-#define TTC_R16_STAGES 3
+// 4 compute warps per CTA and several CTAs per SM (independent pairs in flight, a 4-warp barrier per reduction)
+// measured better than 8 warps per CTA: C2 23.7 M (8 warps, 3 stages, 2 CTAs / SM) -> 26.5 M (4 warps, 3 stages,
+// 2 CTAs) -> 27.3 M pairs/s (4 warps, 2 stages, 3 CTAs); 2 warps per CTA 24.1 M, 1 warp 9.1 M.
+#ifndef TTC_R16_CW
+#define TTC_R16_CW 4
 #endif
-constexpr int kStages = TTC_R16_STAGES;   // TMA ring depth (interior steps in flight per CTA)
+constexpr int kCW = TTC_R16_CW;     // compute warps
+constexpr int kCT = 32 * kCW;       // compute threads
+constexpr int kSlots = 256;         // zfrag slots (2 x 2 fragments x 64)
+constexpr int kSPT = kSlots / kCT;  // slots per compute thread
+static_assert(kSlots % kCT == 0, "slots per thread");
+constexpr int kPart = 2 * 32 * 4;   // floats of one warp's partial Z' (2 n-tiles, fragment-native)
 constexpr int kScrLd = 17;                // row stride of the boundary warp's scratch cores (16 + 1)
 constexpr int kScr = 2 * 16 * kScrLd;     // floats of the scratch
 
@@ -156,6 +161,8 @@ __device__ __forceinline__ void slot_entry(int e, int& zg, int& zf) {
     zf = 8 * kf + (ln & 3) + 4 * jj;
 }
 
+// kStages: TMA ring depth (interior steps in flight per CTA)
+template <int kStages>
 __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Layout lay) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -164,9 +171,9 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
     float* stages = smem;
     float* zpart = smem + kStages * lay.stage_floats;   // [kCW][2 n-tiles][32 lanes][4]
     float* zfrag = zpart + kCW * kPart;           // [slot]: B fragments of Z for the next step
-    float* z1buf = zfrag + kCT;                   // [slot]: Z_1 of the next pair (boundary warp)
-    float* dbuf = z1buf + kCT;                    // [slot]: sum_i X_N[zg,i,0] Y_N[zf,i,0] of the next pair
-    float* scr = lay.scratch ? dbuf + kCT : nullptr;   // boundary warp: two 16 x kScrLd cores (I_1, I_N <= 16)
+    float* z1buf = zfrag + kSlots;                // [slot]: Z_1 of the next pair (boundary warp)
+    float* dbuf = z1buf + kSlots;                 // [slot]: sum_i X_N[zg,i,0] Y_N[zf,i,0] of the next pair
+    float* scr = lay.scratch ? dbuf + kSlots : nullptr;   // boundary warp: two 16 x kScrLd cores (I_1, I_N <= 16)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int N = a.N, I0 = a.dims[0], IL = a.dims[N - 1];
 
@@ -226,7 +233,7 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
                 }
                 __syncwarp();
                 if (k > 0) mbar_wait(&z1empty, (k - 1) & 1);
-                for (int e = lane; e < kCT; e += 32) {
+                for (int e = lane; e < kSlots; e += 32) {
                     int zg, zf;
                     slot_entry(e, zg, zf);
                     const float* xr = scr + zg * kScrLd;
@@ -247,7 +254,7 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
                 }
                 __syncwarp();
                 if (k > 0) mbar_wait(&dempty, (k - 1) & 1);
-                for (int e = lane; e < kCT; e += 32) {
+                for (int e = lane; e < kSlots; e += 32) {
                     int zg, zf;
                     slot_entry(e, zg, zf);
                     const float* xr = scr + zg * kScrLd;
@@ -261,7 +268,7 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
                 continue;
             }
             if (k > 0) mbar_wait(&z1empty, (k - 1) & 1);
-            for (int e = lane; e < kCT; e += 32) {
+            for (int e = lane; e < kSlots; e += 32) {
                 int zg, zf;
                 slot_entry(e, zg, zf);
                 const float* xr = xs + I0 * zg;
@@ -285,7 +292,7 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
             if (k > 0) mbar_wait(&dempty, (k - 1) & 1);
             const float* xl = xs + last;
             const float* yl = ys + last;
-            for (int e = lane; e < kCT; e += 32) {
+            for (int e = lane; e < kSlots; e += 32) {
                 int zg, zf;
                 slot_entry(e, zg, zf);
                 float d = 0.f;
@@ -299,11 +306,16 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
 
     // ------------------------------------------------------------------------------------------ compute
     const int tid = threadIdx.x, lg = lane >> 2, t = lane & 3;
-    // this thread's zfrag slot is tid; its source in a warp's fragment-native partial Zt'[q = zf, s = zg] is the
-    // C fragment of n-tile zg / 8: lane 4 (zf % 8) + (zg % 8) / 2, element 2 (zf / 8) + zg % 2
-    int zg, zf;
-    slot_entry(tid, zg, zf);
-    const int src = ((zg >> 3) * 32 + ((zf & 7) << 2) + ((zg & 7) >> 1)) * 4 + ((zf >> 3) << 1) + (zg & 1);
+    // this thread's zfrag slots are tid + kCT u; the source of slot (zg, zf) in a warp's fragment-native partial
+    // Zt'[q = zf, s = zg] is the C fragment of n-tile zg / 8: lane 4 (zf % 8) + (zg % 8) / 2, element
+    // 2 (zf / 8) + zg % 2
+    int src[kSPT];
+#pragma unroll
+    for (int u = 0; u < kSPT; ++u) {
+        int zg, zf;
+        slot_entry(tid + kCT * u, zg, zf);
+        src[u] = ((zg >> 3) * 32 + ((zf & 7) << 2) + ((zg & 7) >> 1)) * 4 + ((zf >> 3) << 1) + (zg & 1);
+    }
     const int yrow = (lane & 7) + 8 * ((lane >> 3) & 1), ykoff = 4 * (lane >> 4);
 
     int j = 0;
@@ -352,16 +364,23 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
                 *reinterpret_cast<float4*>(zw + (h * 32 + lane) * 4) = make_float4(acc[h][0], acc[h][1], acc[h][2], acc[h][3]);
             bar_named(1, kCT);   // partials visible; every warp is done with zfrag / z1buf
             if (n == 1 && tid == 0) mbar_arrive(&z1empty);
-            float v = 0.f;
+            float vs[kSPT];
 #pragma unroll
-            for (int w = 0; w < kCW; ++w) v += zpart[w * kPart + src];
+            for (int u = 0; u < kSPT; ++u) {
+                vs[u] = 0.f;
+#pragma unroll
+                for (int w = 0; w < kCW; ++w) vs[u] += zpart[w * kPart + src[u]];
+            }
             if (n < N - 2) {
-                zfrag[tid] = v;
+#pragma unroll
+                for (int u = 0; u < kSPT; ++u) zfrag[tid + kCT * u] = vs[u];
                 bar_named(1, kCT);   // next step's B fragments visible; partials free
             } else {
-                // ---- last core: Z_N = sum_{r,p} Z_{N-1}[r,p] D[r,p]; this thread owns Z_{N-1}[zg, zf]
+                // ---- last core: Z_N = sum_{r,p} Z_{N-1}[r,p] D[r,p]; this thread owns its slots of Z_{N-1}
                 mbar_wait(&dfull, k & 1);
-                v *= dbuf[tid];
+                float v = 0.f;
+#pragma unroll
+                for (int u = 0; u < kSPT; ++u) v = fmaf(vs[u], dbuf[tid + kCT * u], v);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 if (lane == 0) red[warp] = v;
@@ -380,36 +399,58 @@ __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Lay
 
 }  // namespace
 
+namespace {
+// Shared-memory bytes of a configuration (without the boundary scratch) and the per-CTA budget at `ctas` per SM
+// (228 KB less 1 KB reserved and ~0.3 KB static shared memory per CTA).
+size_t r16_smem(int stages, int max_dim) {
+    return sizeof(float) * (stages * (size_t)16 * (ps_x(16 * max_dim) + ps_y(16 * max_dim)) + kCW * kPart + 3 * kSlots);
+}
+size_t r16_budget(int ctas) { return (size_t)(228 * 1024 / ctas - 1024 - 320); }
+// (stages, CTAs per SM) in order of preference: 2 stages x 3 CTAs (C2), else 3 x 2, else 2 x 2
+bool r16_config(int max_dim, int* stages, int* ctas) {
+    const int cfg[3][2] = {{2, 3}, {3, 2}, {2, 2}};
+    for (const auto& c : cfg)
+        if (r16_smem(c[0], max_dim) <= r16_budget(c[1])) {
+            *stages = c[0];
+            *ctas = c[1];
+            return true;
+        }
+    return false;
+}
+}  // namespace
+
 bool inner_r16_supported(const InnerArgs& a, bool uniform_r16) {
     if (!uniform_r16 || a.N < 3) return false;
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
-    // two stages of 2 x 16 padded planes + partials + fragments
-    const size_t smem = sizeof(float) * (kStages * (size_t)16 * (ps_x(16 * max_dim) + ps_y(16 * max_dim)) + kCW * kPart + 3 * kCT);
-    return smem <= 112 * 1024;   // two CTAs per SM (the boundary scratch is added only where it still fits)
+    int st, ctas;
+    return r16_config(max_dim, &st, &ctas);
 }
 
 cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s) {
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
+    int stages = 2, ctas = 3;
+    if (!r16_config(max_dim, &stages, &ctas)) return cudaErrorInvalidConfiguration;
     R16Layout lay;
     lay.ps_max = ps_x(16 * max_dim);
     lay.x_floats = 16 * lay.ps_max;
     lay.stage_floats = lay.x_floats + 16 * ps_y(16 * max_dim);
-    size_t smem = sizeof(float) * (kStages * (size_t)lay.stage_floats + kCW * kPart + 3 * kCT);
-    // two CTAs per SM: 228 KB less 1 KB reserved and ~0.2 KB static shared memory per CTA
-    lay.scratch = (a.dims[0] <= 16 && a.dims[a.N - 1] <= 16 && smem + sizeof(float) * kScr <= 113 * 1024) ? 1 : 0;
+    size_t smem = r16_smem(stages, max_dim);
+    // the boundary warp's scratch only where it still fits the budget
+    lay.scratch = (a.dims[0] <= 16 && a.dims[a.N - 1] <= 16 && smem + sizeof(float) * kScr <= r16_budget(ctas)) ? 1 : 0;
     if (lay.scratch) smem += sizeof(float) * kScr;
-    cudaError_t e = cudaFuncSetAttribute(inner_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = stages == 2 ? inner_r16_kernel<2> : inner_r16_kernel<3>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_r16_kernel, 32 * (kCW + 2), smem)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * (kCW + 2), smem)) != cudaSuccess)
         return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int grid = a.B < sms * per_sm ? a.B : sms * per_sm;
-    inner_r16_kernel<<<grid, 32 * (kCW + 2), smem, s>>>(a, lay);
+    kern<<<grid, 32 * (kCW + 2), smem, s>>>(a, lay);
     return cudaGetLastError();
 }
 
