@@ -571,11 +571,87 @@ __device__ double* jacobi_pair(double* G, double* Gn, double* V, int n, JacParam
     return G;
 }
 
-constexpr int kJacPairs = 4;   // eigenproblems per CTA, two warps each
+// The same iteration on ONE warp per eigenproblem (the default; TTC_JAC_PAIR builds use jacobi_pair): each round
+// computes its rotations, applies them to G (block update into Gn) and to V in turn.  Half the registers per
+// problem, so twice as many problems resident per SM: A2's 2,048 eigenproblems per launch fit in one wave
+// (16 per SM) instead of 1.73 (8 per SM), and A2 runs 5% faster (762 K -> 801 K pairs/s) although each problem
+// takes longer.
+__device__ double* jacobi_solo(double* G, double* Gn, double* V, int n, JacParams& P) {
+    const int lane = threadIdx.x & 31;
+    const int np = (n + 1) & ~1, half = np / 2;
+    for (int e = lane; e < n * n; e += 32) V[e] = (e / n == e % n) ? 1.0 : 0.0;   // V transposed (lane = row)
+    int bp[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+        int p = lane + 32 * u, q1 = 0;
+        if (p >= half * (half + 1) / 2) { bp[u] = -1; continue; }
+        while (p >= half - q1) { p -= half - q1; ++q1; }
+        bp[u] = (q1 << 8) | (q1 + p);
+    }
+    int px = lane == 0 ? 0 : lane, py = np - 1 - lane;
+    int sweep = 0, t = 0;
+    bool any = false;
+    for (int r = 0;; ++r) {
+        const int cur = r & 1;
+        bool stop = false;
+        if (t == 0 && r > 0) {
+            stop = !any || sweep == kSweeps;
+            any = false;
+        }
+        if (stop) break;
+        bool rot = false;
+        if (lane < half) {
+            int x = px, y = py;
+            if (x > y) { const int u = x; x = y; y = u; }
+            double c = 1.0, sv = 0.0;
+            if (y < n) {
+                const double app = G[x * n + x], aqq = G[y * n + y], apq = G[x * n + y];
+                if (fabs(apq) > 1e-300 && apq * apq > DBL_EPSILON * DBL_EPSILON * fabs(app * aqq)) {
+                    const double d = aqq - app, b2 = apq + apq;
+                    const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
+                    c = rsqrt(fma(tt, tt, 1.0));
+                    sv = tt * c;
+                    rot = true;
+                }
+            }
+            P.cs[cur][lane] = c; P.sn[cur][lane] = sv; P.pa[cur][lane] = x; P.pb[cur][lane] = y;
+        }
+        const bool rr = __any_sync(0xffffffffu, rot);
+        any |= rr;
+        if (px != 0) px = px == np - 1 ? 1 : px + 1;
+        py = py == np - 1 ? 1 : py + 1;
+        if (++t == np - 1) { t = 0; ++sweep; }
+        if (!rr) continue;
+        __syncwarp();   // the round's parameters visible
+        block_update(G, Gn, n, P, cur, bp);
+        if (lane < n) {
+            for (int q = 0; q < half; ++q) {
+                const int x = P.pa[cur][q], y = P.pb[cur][q];
+                const double sv = P.sn[cur][q];
+                if (y >= n || sv == 0.0) continue;
+                const double c = P.cs[cur][q];
+                const double vx = V[x * n + lane], vy = V[y * n + lane];
+                V[x * n + lane] = c * vx - sv * vy;
+                V[y * n + lane] = sv * vx + c * vy;
+            }
+        }
+        __syncwarp();
+        double* tmp = G; G = Gn; Gn = tmp;
+    }
+    return G;
+}
 
-__global__ void __launch_bounds__(64 * kJacPairs) ttsvd_jacobi_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
+#ifdef TTC_JAC_PAIR
+constexpr int kJacWarps = 2;    // warps per eigenproblem
+#else
+constexpr int kJacWarps = 1;
+#endif
+constexpr int kJacPairs = 4;   // eigenproblems per CTA (kJacWarps warps each)
+
+__global__ void __launch_bounds__(32 * kJacWarps * kJacPairs) ttsvd_jacobi_kernel(const TtsvdArgs a, const TtsvdWs w, int n) {
     extern __shared__ __align__(16) unsigned char sraw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp >> 1, role = warp & 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = kJacWarps == 2 ? warp >> 1 : warp, role = kJacWarps == 2 ? warp & 1 : 0;
     const int b = blockIdx.x * kJacPairs + pair;
     if (b >= a.B) return;   // (both warps of the pair leave: only pair-local barriers below)
     const int g2 = a.gmax * a.gmax, N = a.N;
@@ -596,14 +672,15 @@ __global__ void __launch_bounds__(64 * kJacPairs) ttsvd_jacobi_kernel(const Ttsv
         for (int e = lane; e < side * side; e += 32) G[e] = gsrc[e];
         __syncwarp();
     }
-    const double* Gf = jacobi_pair(G, Gn, V, side, P, role, 1 + pair);
-    if (role == 1) {   // V is final: store it row-major (it was kept transposed)
+    const double* Gf = kJacWarps == 2 ? jacobi_pair(G, Gn, V, side, P, role, 1 + pair) : jacobi_solo(G, Gn, V, side, P);
+    if (kJacWarps == 1) __syncwarp();
+    if (role == 1 || kJacWarps == 1) {   // V is final: store it row-major (it was kept transposed)
         double* vdst = w.v + (int64_t)b * g2;
         for (int e = lane; e < side * side; e += 32) {
             const int k = e / side, x = e - k * side;
             vdst[e] = V[x * side + k];
         }
-        return;
+        if (kJacWarps == 2) return;
     }
     // eigenvalues, descending stable order
     if (lane < side) lam[lane] = fmax(Gf[lane * side + lane], 0.0);
@@ -816,7 +893,7 @@ cudaError_t launch_ttsvd_pipeline(const TtsvdArgs& a, const TtsvdWs& w, cudaStre
     if ((e = cudaFuncSetAttribute(ttsvd_step_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess) return e;
     ttsvd_first_kernel<<<a.B, kThreads, smem_first, s>>>(a, w);
     for (int n = 0; n + 1 < a.N; ++n) {
-        ttsvd_jacobi_kernel<<<(a.B + kJacPairs - 1) / kJacPairs, 64 * kJacPairs, smem_jac, s>>>(a, w, n);
+        ttsvd_jacobi_kernel<<<(a.B + kJacPairs - 1) / kJacPairs, 32 * kJacWarps * kJacPairs, smem_jac, s>>>(a, w, n);
         ttsvd_step_kernel<<<a.B, kThreads, smem_step, s>>>(a, w, n);
     }
     return cudaGetLastError();
