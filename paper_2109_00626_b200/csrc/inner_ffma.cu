@@ -544,7 +544,11 @@ cudaError_t launch_inner_ffma(const InnerArgs& a, int max_rank, bool aligned16, 
     // per SM with rank-32 steps split, measured +8% over 7 warps holding whole steps; 9 warps: -5%)
     const int64_t ring_min = std::max(z.half, (3 * z.step) / 4);
     while (per_sm > 1 && per_sm * cta_bytes(ring_min + fixed) > kSmemPerSM) --per_sm;
-    if (const char* v = std::getenv("TTC_FFMA_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(v)));
+    if (const char* v = std::getenv("TTC_FFMA_PER_SM")) {   // A/B: any count whose ring still holds a split step
+        int want = std::max(1, std::atoi(v));
+        while (want > 1 && want * cta_bytes(z.half + fixed) > kSmemPerSM) --want;
+        per_sm = want;
+    }
     int64_t warp_floats = (((kSmemPerSM / per_sm - kReservedPerCTA) & ~int64_t(255)) / 4);
     warp_floats = std::min<int64_t>(warp_floats, kSmemPerCTA / 4);
     FfArgs w;
