@@ -8,9 +8,10 @@
 //   GEMM-1, per half h (slices i = 2h, 2h+1), M = 128:
 //       D1_h[m = q + 64 i'][r] = sum_p Y_n[p, 2h+i', q] Z[r][p]        (= W_i[r][q], W_i = Z Y_n[:, i, :])
 //       A = the Y_n slice pair as 128 rows x 64 p (a 3-D TMA box: p fastest, then q, then i'), B = Z (64 r x 64 p)
-//   GEMM-2, per slice i, M = 64:
+//   GEMM-2, per slice i, M = 128 (the raw rows and the lo rows of A stacked):
 //       D2[s][q] += sum_r X_n[r, i, s] W_i[r][q]                        (= Z_n after the four slices)
-//       A = X_n[:, i, :]^T as 64 rows s x 64 r (2-D TMA boxes), B = W_i (64 q x 64 r, written by threads)
+//       A = [X_n[:, i, :]^T raw; its lo part] as 128 rows (8-row groups alternating, 2-D TMA boxes of 8 rows s x
+//       32 r), B = W_i (64 q x 64 r, written by threads); a raw row's and its lo row's sums are added by a shuffle
 // 3xTF32: an input core value x (TMA-staged) is fed as its raw bits (the tensor core truncates them to tf32 --
 // measured, tools/tc05_probe.cu) and as lo = RN_tf32(x - trunc_tf32(x)); the operands the threads write (Z, W)
 // as hi = RN_tf32(x) and lo = x - hi; a.b ~ a_hi b_hi + a_lo b_hi + a_hi b_lo with every dropped or rounded term of
@@ -18,12 +19,13 @@
 // sequential fp32 round-to-nearest, tools/tc05_probe.cu).
 //
 // Warp roles (one persistent CTA per SM, pairs assigned statically):
-//   warp 0  TMA producer: 8 tiles of 16 KB per step into a 4-slot ring (+ the pair's boundary cores, 4 KB)
+//   warp 0  TMA producer: 12 ring entries per step (4 Y tiles of 16 KB, 8 X K-chunks of 8 KB) into a 4-slot ring
+//           (+ the pair's boundary cores, 4 KB)
 //   warp 1  TMEM allocator and MMA issuer (one thread)
 //   warps 2-5 epilogue warps (one per TMEM sub-partition): the D1 -> W (hi, lo) and D2 -> Z (hi, lo)
 //            epilogues through tcgen05.ld (partial accumulators summed in fp32), the boundary steps
 //            (Z_1 = A_x^T A_y, Eq. 12, and the final scalar) on the FP32 pipe
-//   warps 6-7 lo workers: the lo parts of the staged input tiles (3-buffer ring)
+//   warps 6-7 lo workers: the lo parts of the staged inputs (Y: 3-buffer lo ring; X: into the entry's own slot)
 #include <cuda.h>
 #include <cstdio>
 
@@ -35,15 +37,25 @@ namespace {
 
 using namespace tc;
 
-constexpr int kTile = 16384;                      // bytes of one staged tile
-constexpr int kRaw = 4, kLo = 3;                  // ring depths (raw input tiles / their lo parts)
+constexpr int kTile = 16384;                      // bytes of one ring slot
+#ifndef TTC_R64TC_RAW
+#define TTC_R64TC_RAW 4
+#endif
+#ifndef TTC_R64TC_LO
+#define TTC_R64TC_LO 3
+#endif
+constexpr int kRaw = TTC_R64TC_RAW, kLo = TTC_R64TC_LO;   // ring depths (staged entries / the Y entries' lo parts)
 #ifndef TTC_R64TC_LO_WARPS
 #define TTC_R64TC_LO_WARPS 2
 #endif
 constexpr int kLoWarps = TTC_R64TC_LO_WARPS;       // lo workers (warps 6 ..); 4 measured 0.94M vs 1.69M pairs/s
                                                    // (168 registers: the epilogue spills)
 constexpr int kThreads = 32 * (6 + kLoWarps);      // TMA, MMA, 4 epilogue warps, the lo workers
-constexpr int kTilesPerStep = 8;                  // Y halves (2 K-chunks each), then X slices 0..3
+// ring entries per interior step: 4 Y tiles (a half's K-chunk: 128 rows x 32 p, 16 KB; its lo part in the lo ring),
+// then 8 X entries (slice i, K-chunk kc: 64 rows s x 32 r, 8 KB) whose lo parts share the slot: 8-row groups
+// alternate raw, lo, raw, lo ... 1 KB each, so that GEMM-2's A operand [X_i^T raw; X_i^T lo] is ONE M = 128
+// operand (8-row groups 1 KB apart) and a raw row and its lo row sit 8 TMEM lanes apart in the same warp
+constexpr int kYPerStep = 4, kEntriesPerStep = 12;
 
 // shared-memory layout (bytes from the 1024-aligned base)
 constexpr int kOffRaw = 0;
@@ -55,13 +67,14 @@ constexpr int kOffB1 = kOffB2 + 4 * kTile;        // Z as the GEMM-1 B operand
 constexpr int kOffBnd = kOffB1 + 2 * kTile;       // 2 buffers x {X_1, Y_1, X_N, Y_N} x 1 KB
 constexpr int kOffRed = kOffBnd + 2 * 4096;       // 4 floats: the final reduction
 constexpr int kOffBar = kOffRed + 64;
-constexpr int kNumBars = 36;
-constexpr int kSmemBytes = kOffBar + 8 * kNumBars + 16 + 1024;   // + TMEM address slot + alignment slack
-
 // barrier indices
-constexpr int FULL = 0, EMPTY = 4, LO_READY = 8, LO_FREE = 12, D1_FULL = 16, D1_EMPTY = 18, B2_READY = 20,
-              B2_FREE = 22, D2_FULL = 24, B1_READY = 25, BND_FULL = 26, BND_EMPTY = 28, D2P_FULL = 30, D2P_EMPTY = 32;
-static_assert(kRaw <= 4 && kLo <= 4, "barrier slots");
+constexpr int FULL = 0, EMPTY = FULL + kRaw, LO_READY = EMPTY + kRaw, LO_FREE = LO_READY + kRaw,
+              D1_FULL = LO_FREE + kLo, D1_EMPTY = D1_FULL + 2, B2_READY = D1_EMPTY + 2, B2_FREE = B2_READY + 2,
+              D2_FULL = B2_FREE + 2, B1_READY = D2_FULL + 1, BND_FULL = B1_READY + 1, BND_EMPTY = BND_FULL + 2,
+              D2P_FULL = BND_EMPTY + 2, D2P_EMPTY = D2P_FULL + 2;
+constexpr int kNumBars = D2P_EMPTY + 2;
+constexpr int kSmemBytes = kOffBar + 8 * kNumBars + 16 + 1024;   // + TMEM address slot + alignment slack
+static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 
 // TMEM columns (512 allocated).  The tensor core's accumulation into TMEM truncates (measured: -5.6e-8 relative per
 // accumulating MMA on positive sums, tools/tc05_probe.cu), so long chains are split: the large a_hi b_hi products
@@ -72,7 +85,8 @@ static_assert(kRaw <= 4 && kLo <= 4, "barrier slots");
 // a_hi [b_hi | b_lo] writes both, one N = 64 MMA adds a_lo b_hi to the second half).
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kD1 = 0;       // + 128 h: GEMM-1 of half h (M = 128)
-constexpr uint32_t kD2 = 256;     // + 128 (i & 1): GEMM-2 of slice i (M = 64), K-chunk kc at lanes 16 kc + (0..15)
+constexpr uint32_t kD2 = 256;     // + 128 (i & 1): GEMM-2 of slice i (M = 128): lane 16 g + e (e < 8) the raw row
+                                  // s = 8 g + e, lane 16 g + 8 + e its lo row; columns 0..63 x b_hi, 64..127 x b_lo
 
 // TTC_R64_PROF builds: clock64 time each role spends in each barrier wait, printed by CTA 0 at the end
 #ifdef TTC_R64_PROF
@@ -197,7 +211,8 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRaw; ++i) { mbar_init(bar_at(sm, FULL + i), 1); mbar_init(bar_at(sm, EMPTY + i), 1); }
-        for (int i = 0; i < kLo; ++i) { mbar_init(bar_at(sm, LO_READY + i), kLoWarps); mbar_init(bar_at(sm, LO_FREE + i), 1); }
+        for (int i = 0; i < kRaw; ++i) mbar_init(bar_at(sm, LO_READY + i), kLoWarps);   // per ring slot
+        for (int i = 0; i < kLo; ++i) mbar_init(bar_at(sm, LO_FREE + i), 1);            // per lo buffer
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar_at(sm, D2P_FULL + i), 1); mbar_init(bar_at(sm, D2P_EMPTY + i), 4);
             mbar_init(bar_at(sm, D1_FULL + i), 1); mbar_init(bar_at(sm, D1_EMPTY + i), 4);
@@ -246,18 +261,19 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                 const int64_t row0 = ((int64_t)c.b * a.pair_elems + 256) / 256;
                 for (int n = 0; n < steps; ++n) {
                     const int row = (int)(row0 + 64 * n);
-                    for (int t = 0; t < kTilesPerStep; ++t, ++k) {
+                    for (int t = 0; t < kEntriesPerStep; ++t, ++k) {
                         const int s = k % kRaw;
                         PW(1, mbar_wait(bar_at(sm, EMPTY + s), ((k / kRaw) & 1) ^ 1));
                         unsigned char* dst = sm + kOffRaw + s * kTile;
                         uint64_t* fb = bar_at(sm, FULL + s);
-                        mbar_arrive_expect_tx(fb, kTile);
-                        if (t < 4) {   // Y half t/2, K-chunk t%2: box (32 p, 2 i, 64 q)
+                        if (t < kYPerStep) {   // Y half t/2, K-chunk t%2: box (32 p, 2 i, 64 q)
+                            mbar_arrive_expect_tx(fb, kTile);
                             tc::tma_3d(dst, &tmy, 32 * (t & 1), row, 2 * (t >> 1), fb);
-                        } else {       // X slice t-4: two boxes (32 r, 64 s)
-                            const int i = t - 4;
-                            tc::tma_2d(dst, &tmx, 64 * i, row, fb);
-                            tc::tma_2d(dst + 8192, &tmx, 64 * i + 32, row, fb);
+                        } else {               // X slice e/2, K-chunk e%2: 8 boxes (32 r, 8 s), raw groups 2 KB apart
+                            const int e = t - kYPerStep;
+                            mbar_arrive_expect_tx(fb, kTile / 2);
+                            for (int g = 0; g < 8; ++g)
+                                tc::tma_2d(dst + 2048 * g, &tmx, 64 * (e >> 1) + 32 * (e & 1), row + 8 * g, fb);
                         }
                     }
                 }
@@ -267,10 +283,9 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
         // ================================================================ MMA issuer
         if (lane == 0) {
             const uint32_t id1w = idesc_tf32(128, 128), id1 = idesc_tf32(128, 64);
-            const uint32_t id2w = idesc_tf32(64, 128), id2 = idesc_tf32(64, 64);
             const uint32_t sbase = smem_u32(sm);
             const uint32_t b1 = sbase + kOffB1;
-            uint32_t k = 0, v = 0;   // tile counter, interior-step counter
+            uint32_t k = 0, v = 0, ky = 0;   // entry counter, interior-step counter, Y-entry counter
             Cursor c;
             for (int it = 0;; ++it) {
                 pair_at(a, it, c);
@@ -283,45 +298,44 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                         const uint32_t d = tmem + kD1 + 128 * h;
                         for (int kc = 0; kc < 2; ++kc, ++k) {
                             PW(4, mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1));
-                            PW(5, mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1));
+                            PW(5, mbar_wait(bar_at(sm, LO_READY + k % kRaw), (k / kRaw) & 1));
                             tc_fence_after();
                             const uint32_t ar = sbase + kOffRaw + (k % kRaw) * kTile;
-                            const uint32_t al = sbase + kOffLo + (k % kLo) * kTile;
+                            const uint32_t al = sbase + kOffLo + (ky % kLo) * kTile;
                             for (int kk = 0; kk < 4; ++kk) {
                                 const uint64_t A = desc_sw128(ar + 32 * kk), Al = desc_sw128(al + 32 * kk);
                                 const uint64_t B = desc_sw128(b1 + 16384 * kc + 32 * kk);   // [Z_hi | Z_lo]
                                 mma_tf32(d, A, B, id1w, (kc | kk) ? 1u : 0u);             // a_hi [b_hi | b_lo]
                                 mma_tf32(d + 64, Al, B, id1, 1u);                         // + a_lo b_hi
                             }
-                            // free this tile's raw slot and lo buffer as soon as its own MMAs are done
+                            // free this entry's slot and lo buffer as soon as its own MMAs are done
                             mma_commit(bar_at(sm, EMPTY + k % kRaw));
-                            mma_commit(bar_at(sm, LO_FREE + k % kLo));
+                            mma_commit(bar_at(sm, LO_FREE + ky % kLo));
+                            ++ky;
                         }
                         mma_commit(bar_at(sm, D1_FULL + h));
                     }
-                    // ---- GEMM-2, slices i = 0..3 (M = 64), accumulated in D2
-                    for (int i = 0; i < 4; ++i, ++k) {
+                    // ---- GEMM-2, slices i = 0..3: one M = 128 MMA per K-block, A = [X_i^T raw; X_i^T lo] (8-row groups
+                    //      interleaved), B = [W_hi | W_lo]: 8 MMAs a slice (16 with an M = 64 raw and a separate lo MMA;
+                    //      the MMA issue is the kernel's pace), each slice's chain 8 MMAs long as in GEMM-1
+                    for (int i = 0; i < 4; ++i) {
                         const int j = i & 1;
-                        PW(6, mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1));
-                        PW(7, mbar_wait(bar_at(sm, LO_READY + k % kLo), (k / kLo) & 1));
                         PW(8, mbar_wait(bar_at(sm, B2_READY + j), (2 * v + (i >> 1)) & 1));
                         PW(9, mbar_wait(bar_at(sm, D2P_EMPTY + j), ((2 * v + (i >> 1)) & 1) ^ 1));
-                        tc_fence_after();
-                        const uint32_t ar = sbase + kOffRaw + (k % kRaw) * kTile;
-                        const uint32_t al = sbase + kOffLo + (k % kLo) * kTile;
                         const uint32_t br = sbase + kOffB2 + j * 2 * kTile;
-                        for (int kc = 0; kc < 2; ++kc) {
-                            const uint32_t d = tmem + kD2 + 128 * j + ((uint32_t)(16 * kc) << 16);
+                        const uint32_t d = tmem + kD2 + 128 * j;
+                        for (int kc = 0; kc < 2; ++kc, ++k) {
+                            PW(6, mbar_wait(bar_at(sm, FULL + k % kRaw), (k / kRaw) & 1));
+                            PW(7, mbar_wait(bar_at(sm, LO_READY + k % kRaw), (k / kRaw) & 1));
+                            tc_fence_after();
+                            const uint32_t ar = sbase + kOffRaw + (k % kRaw) * kTile;
                             for (int kk = 0; kk < 4; ++kk) {
-                                const uint64_t A = desc_sw128(ar + 8192 * kc + 32 * kk);
-                                const uint64_t Al = desc_sw128(al + 8192 * kc + 32 * kk);
+                                const uint64_t A = desc_sw128(ar + 32 * kk);
                                 const uint64_t B = desc_sw128(br + 16384 * kc + 32 * kk);   // [W_hi | W_lo]
-                                mma_tf32(d, A, B, id2w, kk ? 1u : 0u);
-                                mma_tf32(d + 64, Al, B, id2, 1u);
+                                mma_tf32(d, A, B, id1w, (kc | kk) ? 1u : 0u);
                             }
+                            mma_commit(bar_at(sm, EMPTY + k % kRaw));
                         }
-                        mma_commit(bar_at(sm, EMPTY + k % kRaw));
-                        mma_commit(bar_at(sm, LO_FREE + k % kLo));
                         mma_commit(bar_at(sm, B2_FREE + j));
                         mma_commit(bar_at(sm, D2P_FULL + j));
                     }
@@ -335,24 +349,42 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
         constexpr int kLoT = 32 * kLoWarps;       // lo threads
         const int ct = threadIdx.x - 192;         // 0 .. kLoT - 1
         uint32_t ktot = 0;
-        for (int idx = blockIdx.x; idx < a.B; idx += gridDim.x) ktot += (uint32_t)steps * kTilesPerStep;
+        for (int idx = blockIdx.x; idx < a.B; idx += gridDim.x) ktot += (uint32_t)steps * kEntriesPerStep;
+        uint32_t ky = 0;
         for (uint32_t k = 0; k < ktot; ++k) {
-            const int s = k % kRaw, l = k % kLo;
+            const int s = k % kRaw;
             PW(10, mbar_wait(bar_at(sm, FULL + s), (k / kRaw) & 1));
-            PW(11, mbar_wait(bar_at(sm, LO_FREE + l), ((k / kLo) & 1) ^ 1));
             const float4* src = reinterpret_cast<const float4*>(sm + kOffRaw + s * kTile);
-            float4* dst = reinterpret_cast<float4*>(sm + kOffLo + l * kTile);
+            if ((k % kEntriesPerStep) < kYPerStep) {   // Y entry: its 16 KB lo part into the lo ring (same layout)
+                const int l = ky % kLo;
+                PW(11, mbar_wait(bar_at(sm, LO_FREE + l), ((ky / kLo) & 1) ^ 1));
+                ++ky;
+                float4* dst = reinterpret_cast<float4*>(sm + kOffLo + l * kTile);
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                float4 r[kTile / 16 / (2 * kLoT)];
+                for (int hf = 0; hf < 2; ++hf) {
+                    float4 r[kTile / 16 / (2 * kLoT)];
 #pragma unroll
-                for (int e = 0; e < kTile / 16 / (2 * kLoT); ++e) r[e] = src[ct + kLoT * (2 * e + hf)];
+                    for (int e = 0; e < kTile / 16 / (2 * kLoT); ++e) r[e] = src[ct + kLoT * (2 * e + hf)];
 #pragma unroll
-                for (int e = 0; e < kTile / 16 / (2 * kLoT); ++e) dst[ct + kLoT * (2 * e + hf)] = lo_rn4(r[e]);
+                    for (int e = 0; e < kTile / 16 / (2 * kLoT); ++e) dst[ct + kLoT * (2 * e + hf)] = lo_rn4(r[e]);
+                }
+            } else {   // X entry: raw group g (1 KB at 2 KB g) -> lo group g at 2 KB g + 1 KB (same swizzle phase)
+                float4 r[kTile / 32 / kLoT];
+#pragma unroll
+                for (int e = 0; e < kTile / 32 / kLoT; ++e) {
+                    const int q = ct + kLoT * e;                     // float4 index within the 8 KB of raw data
+                    r[e] = src[((q >> 6) << 7) + (q & 63)];
+                }
+                float4* dst = reinterpret_cast<float4*>(sm + kOffRaw + s * kTile) + 64;
+#pragma unroll
+                for (int e = 0; e < kTile / 32 / kLoT; ++e) {
+                    const int q = ct + kLoT * e;
+                    dst[((q >> 6) << 7) + (q & 63)] = lo_rn4(r[e]);
+                }
             }
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_at(sm, LO_READY + l));
+            if (lane == 0) mbar_arrive(bar_at(sm, LO_READY + s));
         }
     } else {
         // ================================================================ epilogue warps (warps 2..5)
@@ -413,7 +445,8 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                         write_b32(sm + kOffB2 + ip * 2 * kTile, q, 32 * hh, f);
                     }
                 };
-                // GEMM-2 slice partials: lanes 0..15 accumulate K-chunk 0, lanes 16..31 K-chunk 1 of row 16 sp + lane % 16
+                // GEMM-2 slice sums of TMEM lane 32 sp + lane: the raw row s (lane bit 3 clear) or the lo row of s (set),
+                // s = 16 sp + 8 (lane >> 4) + lane % 8
                 float zacc[64];
                 auto add_slice = [&](int i) {
                     const int j = i & 1;
@@ -465,18 +498,17 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                 }
                 add_slice(2);
                 add_slice(3);
-                // ---- epilogue 2: Z_n = (chunk-0 sums + chunk-1 sums) + cross terms (rows s = 16 sp + lane, lane < 16)
+                // ---- epilogue 2: Z_n row s = raw-row sums + lo-row sums (lanes 8 apart)
                 uint32_t z0[32], z1[32];     // (slice 3 read above: every MMA of the step is complete)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
-                    z0[e] = __float_as_uint(zacc[e] + __shfl_xor_sync(0xffffffffu, zacc[e], 16));
-                    z1[e] = __float_as_uint(zacc[32 + e] + __shfl_xor_sync(0xffffffffu, zacc[32 + e], 16));
+                    z0[e] = __float_as_uint(zacc[e] + __shfl_xor_sync(0xffffffffu, zacc[e], 8));
+                    z1[e] = __float_as_uint(zacc[32 + e] + __shfl_xor_sync(0xffffffffu, zacc[32 + e], 8));
                 }
-                // lanes t and t + 16 now both hold row 16 sp + t (chunk-0 + chunk-1 partial sums): lane t writes its
-                // columns 0..31, lane t + 16 columns 32..63 (the whole warp stores)
-                const int s = 16 * sp + (lane & 15);
+                // both lanes of a pair now hold row s: the raw lane writes its columns 0..31, the lo lane 32..63
+                const int s = 16 * sp + 8 * (lane >> 4) + (lane & 7);
+                const bool upper = (lane & 8) != 0;
                 if (n + 1 < steps) {
-                    const bool upper = lane >= 16;
                     float4 f[8];
 #pragma unroll
                     for (int c4 = 0; c4 < 8; ++c4) f[c4] = sel4(upper, f4(z1 + 4 * c4), f4(z0 + 4 * c4));
@@ -485,23 +517,24 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bar_at(sm, B1_READY));
                 } else {
-                    // ---- last step: out = sum_{s,q} Z[s][q] sum_i X_N[s, i, 0] Y_N[q, i, 0]
+                    // ---- last step: out = sum_{s,q} Z[s][q] sum_i X_N[s, i, 0] Y_N[q, i, 0] (each lane of a pair
+                    //      takes half of row s's columns)
                     float acc = 0.f;
-                    if (lane < 16) {
+                    {
                         const float* xN = bnd + 512;
-                        const float* yN = bnd + 768;
+                        const float* yN = bnd + 768 + (upper ? 32 : 0);
                         const float x0 = xN[s], x1 = xN[s + 64], x2 = xN[s + 128], x3 = xN[s + 192];
 #pragma unroll
-                        for (int qq = 0; qq < 64; ++qq) {
+                        for (int qq = 0; qq < 32; ++qq) {
                             float t = x0 * yN[qq];
                             t = fmaf(x1, yN[qq + 64], t);
                             t = fmaf(x2, yN[qq + 128], t);
                             t = fmaf(x3, yN[qq + 192], t);
-                            acc = fmaf(__uint_as_float(qq < 32 ? z0[qq & 31] : z1[qq & 31]), t, acc);
+                            acc = fmaf(__uint_as_float(upper ? z1[qq] : z0[qq]), t, acc);
                         }
                     }
 #pragma unroll
-                    for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                     if (lane == 0) red[sp] = acc;
                     bar_named(1, 128);
                     if (ct == 0) a.out[c.b] = (red[0] + red[1]) + (red[2] + red[3]);
@@ -556,10 +589,10 @@ cudaError_t launch_inner_r64tc(const InnerArgs& a, cudaStream_t s) {
     const int64_t pe = a.x.train_elems;            // 256 + (N - 2) 16384 + 256 floats per train
     const cuuint64_t rows = (cuuint64_t)((int64_t)a.B * pe / 256);
     CUtensorMap tmx, tmy;
-    {   // X: rows of 256 floats (r + 64 i for one s), box 32 x 64 rows
+    {   // X: rows of 256 floats (r + 64 i for one s), box 32 x 8 rows (one 8-row group of an X entry)
         const cuuint64_t dims[2] = {256, rows};
         const cuuint64_t strides[1] = {1024};
-        const cuuint32_t box[2] = {32, 64};
+        const cuuint32_t box[2] = {32, 8};
         const cuuint32_t es[2] = {1, 1};
         if (enc(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.x.cores), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
