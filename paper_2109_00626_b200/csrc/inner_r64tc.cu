@@ -269,11 +269,10 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
                         if (t < kYPerStep) {   // Y half t/2, K-chunk t%2: box (32 p, 2 i, 64 q)
                             mbar_arrive_expect_tx(fb, kTile);
                             tc::tma_3d(dst, &tmy, 32 * (t & 1), row, 2 * (t >> 1), fb);
-                        } else {               // X slice e/2, K-chunk e%2: 8 boxes (32 r, 8 s), raw groups 2 KB apart
-                            const int e = t - kYPerStep;
+                        } else {               // X slice e/2, K-chunk e%2: one box (32 r, 64 s) into the slot's first
+                            const int e = t - kYPerStep;   // 8 KB (the lo workers spread the 8-row groups)
                             mbar_arrive_expect_tx(fb, kTile / 2);
-                            for (int g = 0; g < 8; ++g)
-                                tc::tma_2d(dst + 2048 * g, &tmx, 64 * (e >> 1) + 32 * (e & 1), row + 8 * g, fb);
+                            tc::tma_2d(dst, &tmx, 64 * (e >> 1) + 32 * (e & 1), row, fb);
                         }
                     }
                 }
@@ -368,18 +367,20 @@ inner_r64tc_kernel(const TcArgs a, const __grid_constant__ CUtensorMap tmx, cons
 #pragma unroll
                     for (int e = 0; e < kTile / 16 / (2 * kLoT); ++e) dst[ct + kLoT * (2 * e + hf)] = lo_rn4(r[e]);
                 }
-            } else {   // X entry: raw group g (1 KB at 2 KB g) -> lo group g at 2 KB g + 1 KB (same swizzle phase)
+            } else {   // X entry: the 8 KB raw box (64 rows) read whole, then raw 8-row group g rewritten at 2 KB g and
+                       // its lo part at 2 KB g + 1 KB (1 KB swizzle atoms: the swizzle phase is kept)
                 float4 r[kTile / 32 / kLoT];
+#pragma unroll
+                for (int e = 0; e < kTile / 32 / kLoT; ++e) r[e] = src[ct + kLoT * e];
+                __syncwarp();
+                bar_named(2, kLoT);   // every lo thread has read the box before any group moves
+                float4* dst = reinterpret_cast<float4*>(sm + kOffRaw + s * kTile);
 #pragma unroll
                 for (int e = 0; e < kTile / 32 / kLoT; ++e) {
                     const int q = ct + kLoT * e;                     // float4 index within the 8 KB of raw data
-                    r[e] = src[((q >> 6) << 7) + (q & 63)];
-                }
-                float4* dst = reinterpret_cast<float4*>(sm + kOffRaw + s * kTile) + 64;
-#pragma unroll
-                for (int e = 0; e < kTile / 32 / kLoT; ++e) {
-                    const int q = ct + kLoT * e;
-                    dst[((q >> 6) << 7) + (q & 63)] = lo_rn4(r[e]);
+                    const int o = ((q >> 6) << 7) + (q & 63);
+                    dst[o] = r[e];
+                    dst[o + 64] = lo_rn4(r[e]);
                 }
             }
             fence_proxy_async();
@@ -589,10 +590,10 @@ cudaError_t launch_inner_r64tc(const InnerArgs& a, cudaStream_t s) {
     const int64_t pe = a.x.train_elems;            // 256 + (N - 2) 16384 + 256 floats per train
     const cuuint64_t rows = (cuuint64_t)((int64_t)a.B * pe / 256);
     CUtensorMap tmx, tmy;
-    {   // X: rows of 256 floats (r + 64 i for one s), box 32 x 8 rows (one 8-row group of an X entry)
+    {   // X: rows of 256 floats (r + 64 i for one s), box 32 x 64 rows (one K-chunk of one slice)
         const cuuint64_t dims[2] = {256, rows};
         const cuuint64_t strides[1] = {1024};
-        const cuuint32_t box[2] = {32, 8};
+        const cuuint32_t box[2] = {32, 64};
         const cuuint32_t es[2] = {1, 1};
         if (enc(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.x.cores), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
