@@ -161,8 +161,8 @@ __device__ __forceinline__ void slot_entry(int e, int& zg, int& zf) {
     zf = 8 * kf + (ln & 3) + 4 * jj;
 }
 
-// kStages: TMA ring depth (interior steps in flight per CTA)
-template <int kStages>
+constexpr int kStages = 2;   // TMA ring depth (interior steps in flight per CTA)
+
 __global__ void __maxnreg__(96) inner_r16_kernel(const InnerArgs a, const R16Layout lay) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -406,13 +406,12 @@ size_t r16_smem(int stages, int max_dim) {
     return sizeof(float) * (stages * (size_t)16 * (ps_x(16 * max_dim) + ps_y(16 * max_dim)) + kCW * kPart + 3 * kSlots);
 }
 size_t r16_budget(int ctas) { return (size_t)(228 * 1024 / ctas - 1024 - 320); }
-// (stages, CTAs per SM) in order of preference: 2 stages x 3 CTAs (C2), else 3 x 2, else 2 x 2
-bool r16_config(int max_dim, int* stages, int* ctas) {
-    const int cfg[3][2] = {{2, 3}, {3, 2}, {2, 2}};
-    for (const auto& c : cfg)
-        if (r16_smem(c[0], max_dim) <= r16_budget(c[1])) {
-            *stages = c[0];
-            *ctas = c[1];
+// CTAs per SM with the 2-stage ring: 3 (mode sizes <= 16, C2), else 2 (<= 26); a 3-stage ring at 2 CTAs per SM
+// never fits where 2 stages at 3 do not
+bool r16_config(int max_dim, int* ctas) {
+    for (int c = 3; c >= 2; --c)
+        if (r16_smem(kStages, max_dim) <= r16_budget(c)) {
+            *ctas = c;
             return true;
         }
     return false;
@@ -423,24 +422,24 @@ bool inner_r16_supported(const InnerArgs& a, bool uniform_r16) {
     if (!uniform_r16 || a.N < 3) return false;
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
-    int st, ctas;
-    return r16_config(max_dim, &st, &ctas);
+    int ctas;
+    return r16_config(max_dim, &ctas);
 }
 
 cudaError_t launch_inner_r16(const InnerArgs& a, cudaStream_t s) {
     int max_dim = 1;
     for (int n = 0; n < a.N; ++n) max_dim = a.dims[n] > max_dim ? a.dims[n] : max_dim;
-    int stages = 2, ctas = 3;
-    if (!r16_config(max_dim, &stages, &ctas)) return cudaErrorInvalidConfiguration;
+    int ctas = 3;
+    if (!r16_config(max_dim, &ctas)) return cudaErrorInvalidConfiguration;
     R16Layout lay;
     lay.ps_max = ps_x(16 * max_dim);
     lay.x_floats = 16 * lay.ps_max;
     lay.stage_floats = lay.x_floats + 16 * ps_y(16 * max_dim);
-    size_t smem = r16_smem(stages, max_dim);
+    size_t smem = r16_smem(kStages, max_dim);
     // the boundary warp's scratch only where it still fits the budget
     lay.scratch = (a.dims[0] <= 16 && a.dims[a.N - 1] <= 16 && smem + sizeof(float) * kScr <= r16_budget(ctas)) ? 1 : 0;
     if (lay.scratch) smem += sizeof(float) * kScr;
-    auto kern = stages == 2 ? inner_r16_kernel<2> : inner_r16_kernel<3>;
+    auto kern = inner_r16_kernel;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;

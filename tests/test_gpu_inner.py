@@ -211,11 +211,12 @@ def test_edge_shapes():
 
 
 @pytest.mark.parametrize("dims", [(16, 16), (4, 16, 16), (16, 16, 16), (3, 5, 16, 7, 2), (13, 9, 11, 1),
-                                  (1, 8, 1, 8, 1, 8), (6, 12, 16, 10, 14, 4, 2)])
+                                  (1, 8, 1, 8, 1, 8), (6, 12, 16, 10, 14, 4, 2), (20, 20, 20), (3, 24, 5, 26, 2)])
 def test_uniform_rank16_shapes(dims):
     """The uniform rank-16 kernel (first / last cores from L2, interior cores through the TMA ring) on mixed
     mode sizes: fewer slices than warps, odd slice counts, I = 1 cores, boundary I not a multiple of 4, a single
-    interior core (N = 3), and N = 2 (no interior core: served by another kernel)."""
+    interior core (N = 3), N = 2 (no interior core: served by another kernel), and mode sizes 17..26 (2 CTAs per
+    SM instead of 3; with I_1 = I_N = 20 the boundary warp reads its cores from global memory, no scratch)."""
     rng = np.random.default_rng(sum(dims))
     B = 37
     N = len(dims)
