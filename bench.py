@@ -384,7 +384,7 @@ def make_work(ttc, cfg, b0, B, seed, dev, stream, ranks=None):
 
         def step():
             ttc.ttc_inner(XD, YD, out=out, stream=stream, order=order)
-        w.kernel = {"C1": "inner_small_kernel", "C2": "inner_r16_kernel", "C4": "inner_r64_kernel",
+        w.kernel = {"C1": "inner_small_kernel", "C2": "inner_r16_kernel", "C4": "inner_r64tc_kernel",
                     "C5": "inner_ffma_kernel"}.get(cfg, "inner")
     w.step, w.out = step, out
     w.xin = X.cores if hasattr(X, "cores") else X
