@@ -624,15 +624,17 @@ __device__ double* jacobi_solo(double* G, double* Gn, double* V, int n, JacParam
         if (!rr) continue;
         __syncwarp();   // the round's parameters visible
         block_update(G, Gn, n, P, cur, bp);
-        if (lane < n) {
-            for (int q = 0; q < half; ++q) {
+        {   // V J: the round's (rotation q, row) items spread over all 32 lanes (rotations touch disjoint row pairs
+            // of the transposed V; identity rotations rewrite their rows unchanged); e / n by a multiply-shift
+            const unsigned inv = (65536u + (unsigned)n - 1u) / (unsigned)n;   // exact for e < 1024 when n <= 32
+            for (int e = lane; e < half * n; e += 32) {
+                const int q = (int)(((unsigned)e * inv) >> 16), row = e - q * n;
                 const int x = P.pa[cur][q], y = P.pb[cur][q];
-                const double sv = P.sn[cur][q];
-                if (y >= n || sv == 0.0) continue;
-                const double c = P.cs[cur][q];
-                const double vx = V[x * n + lane], vy = V[y * n + lane];
-                V[x * n + lane] = c * vx - sv * vy;
-                V[y * n + lane] = sv * vx + c * vy;
+                if (y >= n) continue;
+                const double c = P.cs[cur][q], sv = P.sn[cur][q];
+                const double vx = V[x * n + row], vy = V[y * n + row];
+                V[x * n + row] = c * vx - sv * vy;
+                V[y * n + row] = sv * vx + c * vy;
             }
         }
         __syncwarp();
