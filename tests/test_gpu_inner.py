@@ -361,18 +361,19 @@ def test_graph_replay_and_concurrent_streams_are_reentrant():
             assert torch.equal(outs[k], ref[k]), (rep, k)
 
 
-@pytest.mark.parametrize("case", ["c5", "gaps", "dims"])
+@pytest.mark.parametrize("case", ["c5", "gaps", "dims", "i1", "i3"])
 def test_ffma_tma_staging_matches_cp_async(monkeypatch, case):
     """The FP32 kernel's two staging paths (TMA tensor boxes with zero-filled padding, TTC_FFMA_TMA=1, vs 16-byte
     cp.async, TTC_FFMA_TMA=0) stage the same values, so the results are bitwise equal: C5 correlated pairs; trains
     at gapped offsets (16-byte steps) with the last core ending at the buffer's end; mixed interior mode sizes
     (several G run lengths).  Both paths are also checked against the oracle."""
-    rng = np.random.default_rng({"c5": 1, "gaps": 2, "dims": 3}[case])
+    rng = np.random.default_rng({"c5": 1, "gaps": 2, "dims": 3, "i1": 4, "i3": 5}[case])
     if case == "c5":
         X, Y = ttgen.config_batch("C5", kind="corr", B=300)
         XD, YD = ttc.TTDevice.from_batch(X, DEV), ttc.TTDevice.from_batch(Y, DEV)
     else:
-        dims = (2,) * 12 if case == "gaps" else (2, 3, 2, 3, 2, 2)   # 8 run lengths: a full map table
+        dims = {"gaps": (2,) * 12, "dims": (2, 3, 2, 3, 2, 2),   # 8 run lengths: a full map table
+                "i1": (2, 1, 1, 1, 1, 2), "i3": (1, 3, 3, 3, 1)}[case]   # G runs of Ga (I = 1) / 3 Ga floats
         B, N = 97, len(dims)
         def ranks():
             r = rng.choice([8, 16, 24, 32], size=(B, N + 1)).astype(np.int32)
