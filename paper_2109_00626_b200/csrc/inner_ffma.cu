@@ -292,6 +292,15 @@ __device__ __forceinline__ void fc_pop(const InnerArgs& a, const FfArgs&, FCurso
         rk[N + 1 + n] = frank(a.y, c.b, N, n);
     }
     __syncwarp();
+    // the association of every interior step at once (bit n of vfm: step n is V-first), one ballot per 32 steps
+    unsigned* vfm = reinterpret_cast<unsigned*>(rk + 2 * (N + 1));
+    for (int n0 = 0; n0 < N; n0 += 32) {
+        const int n = n0 + lane;
+        const bool v = n >= 1 && n + 1 < N && vfirst(rk[n], rk[N + 1 + n], rk[n + 1], rk[N + 2 + n]);
+        const unsigned m = __ballot_sync(0xffffffffu, v);
+        if (lane == 0) vfm[n0 >> 5] = m;
+    }
+    __syncwarp();
     c.n = 0;
     c.half = false;
     c.R = 1;
@@ -313,6 +322,7 @@ inner_ffma_kernel(const InnerArgs a, const FfArgs w, const __grid_constant__ FfM
     uint64_t* bars = reinterpret_cast<uint64_t*>(q + kQ);   // kTma: one mbarrier per queue entry
     int* rk = reinterpret_cast<int*>(bars + kQ);
     const int N = a.N;
+    const unsigned* vfm = reinterpret_cast<const unsigned*>(rk + 2 * (N + 1));   // fc_pop's association bits
     unsigned phase = 0;                                      // kTma: parity bit per queue entry
     if (kTma) {
         if (lane == 0) {
@@ -339,7 +349,7 @@ inner_ffma_kernel(const InnerArgs a, const FfArgs w, const __grid_constant__ FfM
                 need = ((R * I * S + 3) & ~3) + ((P * I * Q + 3) & ~3);
                 if (kTma) need = (need + 31) & ~31;   // every step starts on 128 bytes (TMA destinations)
             } else {
-                vf = vfirst(R, P, S, Q);
+                vf = (vfm[n >> 5] >> (n & 31)) & 1u;
                 const int Fa = vf ? R : P, Fb = vf ? S : Q, Ga = vf ? P : R, Gb = vf ? Q : S;
                 const int needF = I * Fb * (Fa + kPad), needG = Gb * (Ga * I + kPad);
                 need = needF + needG;
@@ -386,7 +396,7 @@ inner_ffma_kernel(const InnerArgs a, const FfArgs w, const __grid_constant__ FfM
             }
             tc::cp_commit_group();
             int znext = 0;   // the next step's Z orientation (the last step reads [r][p])
-            if (n + 1 < N - 1) znext = vfirst(S, Q, rk[n + 2], rk[N + 3 + n]);
+            if (n + 1 < N - 1) znext = (vfm[(n + 1) >> 5] >> ((n + 1) & 31)) & 1u;
             if (lane == 0) {
                 FStep f;
                 f.start = (int)start_off;
@@ -459,7 +469,7 @@ FfSizes ffma_sizes(int max_rank, int max_dim, int N) {
     z.half = std::max(I * r * (r + kPad), r * (r * I + kPad)) + 64;   // its larger operand (a split step)
     z.zbuf = r * (r + kPad);
     z.wbuf = r * (r * I + kPad);
-    z.qf = (kQ * (int64_t)sizeof(FStep) / 4 + 2 * kQ + 2 * (N + 1) + 3) & ~int64_t(3);
+    z.qf = (kQ * (int64_t)sizeof(FStep) / 4 + 2 * kQ + 2 * (N + 1) + (N + 31) / 32 + 3) & ~int64_t(3);
     return z;
 }
 constexpr int64_t kSmemPerSM = 228 * 1024, kSmemPerCTA = 227 * 1024, kReservedPerCTA = 1024;
