@@ -14,9 +14,11 @@
 // layout (Eq. 2), so each lane loads 4 K-values with one 16-byte LDS and does 4 FFMA per output it owns.
 // Lane (lg = lane / 4, lf = lane % 4) owns rows lg + 8a and columns lf + 4b of each output tile.
 //
-// Staging: the warp copies its own future steps into a private ring with 16-byte cp.async, inserting 4 floats
-// of padding after every contiguous run (F: runs of Fa, G: runs of Ga*I) so that the 8 (or 4) distinct runs
-// one LDS.128 touches fall into distinct bank groups; Z and W are kept with padded row strides likewise.
+// Staging: the warp copies its own future steps into a private ring, with 4 floats of padding after every
+// contiguous run (F: runs of Fa, G: runs of Ga*I) so that the 8 (or 4) distinct runs one LDS.128 touches fall into
+// distinct bank groups -- interior operands by TMA tensor boxes (FfMaps below: the padding is the out-of-range
+// tail of each box row, zero-filled), boundary cores and batches whose run lengths overflow the map table by
+// 16-byte cp.async; Z and W are kept with padded row strides likewise.
 // Pairs are assigned statically: warp w of W takes positions w, 2W-1-w, 2W+w, 4W-1-w, ... of the work list
 // (a "snake" over the cost-descending list of ttc_inner_ordered balances heterogeneous pairs); no global state,
 // so concurrent launches and graph replays on several streams are independent (re-entrant, ttc.h).

@@ -1,7 +1,7 @@
 // inner_r16.cu -- tt_inner specialised for batches whose trains all have the rank profile (1, 16, ..., 16, 1)
 // (BASELINE.json C2: N = 8, I = 16, R = 16).  Same sweep as ttc.h / inner_fast.cu:
 //   Z_0 = [1],  Z_n = sum_i X_n[:, i, :]^T Z_{n-1} Y_n[:, i, :],  out = Z_N.
-// Persistent CTAs (two per SM), warp-specialised:
+// Persistent CTAs (three per SM for mode sizes up to 16, two up to 26: three pairs in flight per SM), warp-specialised:
 //   * producer warp: TMA bulk copies (cp.async.bulk) of each INTERIOR step's two cores into a kStages-deep ring
 //     (one copy per plane into padded planes), full/empty mbarriers;
 //   * boundary warp: the two rank-1 cores of each pair (1 KB per core and train for I = 16 -- as a ring stage
@@ -9,7 +9,7 @@
 //     one short step ahead of its use), one pair ahead, on the FP32 pipe from global memory:
 //       Z_1[s, q] = sum_i X_1[0,i,s] Y_1[0,i,q]   (Eq. 12's K = A_x^T A_y), in B-fragment slot order;
 //       D[r, p]   = sum_i X_N[r,i,0] Y_N[p,i,0],  so that  Z_N = sum_{r,p} Z_{N-1}[r,p] D[r,p];
-//   * 8 compute warps: per interior step the two rank-16 GEMMs of each slice i on the tensor cores (3xTF32
+//   * 4 compute warps: per interior step the two rank-16 GEMMs of each slice i on the tensor cores (3xTF32
 //     mma.sync m16n8k8, ldmatrix for the Y operand, every bound a compile-time constant), slices spread over
 //     the warps, partials reduced through shared memory in a fixed order into the next step's B fragments; the
 //     last interior step's reduction is fused with the last core (multiply by D, fixed-order block reduction).
