@@ -244,7 +244,9 @@ __device__ __forceinline__ void ff_step2(int Fb, const float* G, int Ga, int Gb,
 
 // First step (R = P = 1): Z_1[s, q] = sum_i X_1[0, i, s] Y_1[0, i, q] -- Eq. 12's K -- stored for the next step:
 // znext = 0: Z[s][q] stride Q + kPad, znext = 1: Z[q][s] stride S + kPad.
-__device__ __forceinline__ void ff_first(const float* X, const float* Y, int S, int Q, int I, int znext, float* Z,
+// (The two boundary steps run once per pair: kept out of line, so that the steady-state step loop stays compact in
+// the instruction caches -- measured +4.5% on C5.)
+__device__ __noinline__ void ff_first(const float* X, const float* Y, int S, int Q, int I, int znext, float* Z,
                                          int lane) {
     for (int q = 0; q < Q; ++q)
         for (int s = lane; s < S; s += 32) {
@@ -256,7 +258,7 @@ __device__ __forceinline__ void ff_first(const float* X, const float* Y, int S, 
 }
 // Last step (S = Q = 1): Z_N = sum_{r,p} Z[r,p] sum_i X_N[r,i,0] Y_N[p,i,0], Z[r][p] stride P + kPad (first:
 // N = 1, Z_0 = 1).  Warp-reduced in a fixed order.
-__device__ __forceinline__ float ff_last(const float* X, const float* Y, int R, int P, int I, bool first, const float* Z,
+__device__ __noinline__ float ff_last(const float* X, const float* Y, int R, int P, int I, bool first, const float* Z,
                                          int lane) {
     float v = 0.f;
     for (int p = 0; p < P; ++p)
