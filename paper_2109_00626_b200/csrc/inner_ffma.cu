@@ -116,6 +116,7 @@ __device__ __forceinline__ void stage_padded(float* dst, const float* src, int r
     const unsigned q = (unsigned)run >> 2;
     const unsigned div = c_magic.v[q];
     const unsigned chunks = (unsigned)runs * q;
+#pragma unroll 1
     for (unsigned e = lane; e < chunks; e += 32) {
         const unsigned c = __umulhi(e, div);
         const unsigned o = e - c * q;
@@ -124,8 +125,10 @@ __device__ __forceinline__ void stage_padded(float* dst, const float* src, int r
 }
 __device__ __forceinline__ void stage_plain(float* dst, const float* src, int n, int lane) {
     if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+#pragma unroll 1
         for (int e = 4 * lane; e < n; e += 128) tc::cp_async16(dst + e, src + e);
     } else {   // odd boundary sizes (N = 1, I odd): plain copies, visible after the consumer's __syncwarp
+#pragma unroll 1
         for (int e = lane; e < n; e += 32) dst[e] = __ldg(src + e);
     }
 }
@@ -248,6 +251,7 @@ __device__ __forceinline__ void ff_step2(int Fb, const float* G, int Ga, int Gb,
 // the instruction caches -- measured +4.5% on C5.)
 __device__ __noinline__ void ff_first(const float* X, const float* Y, int S, int Q, int I, int znext, float* Z,
                                          int lane) {
+#pragma unroll 1
     for (int q = 0; q < Q; ++q)
         for (int s = lane; s < S; s += 32) {
             float d = 0.f;
@@ -382,6 +386,8 @@ inner_ffma_kernel(const InnerArgs a, const FfArgs w, const __grid_constant__ FfM
                     if (lane == 0) tc::mbar_arrive_expect_tx(bar, 4u * (unsigned)tx);
                     __syncwarp();
                     const int nf = part != 2 ? (I * Fb) >> 3 : 0, ng = part != 1 ? Gb >> 3 : 0;
+                    // (staging loops are kept rolled: a compact step loop in the instruction caches, +2% on C5)
+#pragma unroll 1
                     for (int j = lane; j < nf + ng; j += 32) {
                         const bool isF = j < nf;
                         const int jj = isF ? j : j - nf, L = isF ? Fa : Ga * I;
