@@ -451,14 +451,9 @@ inner_ffma_kernel(const InnerArgs a, const FfArgs w, const __grid_constant__ FfM
         } else {
             const int vf = f.vf;
             const int Fa = vf ? f.R : f.P, Fb = vf ? f.S : f.Q, Ga = vf ? f.P : f.R, Gb = vf ? f.Q : f.S;
-            if (f.part == 0) {
-                ff_step1(X, Fa, Fb, Ga, f.I, Z, W, lane);
-                ff_step2(Fb, X + f.I * Fb * (Fa + kPad), Ga, Gb, f.I, Z, W, f.znext != vf, lane);
-            } else if (f.part == 1) {
-                ff_step1(X, Fa, Fb, Ga, f.I, Z, W, lane);
-            } else {
-                ff_step2(Fb, X, Ga, Gb, f.I, Z, W, f.znext != vf, lane);
-            }
+            // one call site per GEMM (part 0: both, 1: GEMM-1 on F, 2: GEMM-2 on G staged alone)
+            if (f.part != 2) ff_step1(X, Fa, Fb, Ga, f.I, Z, W, lane);
+            if (f.part != 1) ff_step2(Fb, f.part == 2 ? X : X + f.I * Fb * (Fa + kPad), Ga, Gb, f.I, Z, W, f.znext != vf, lane);
         }
         __syncwarp();
         tail = f.end;
