@@ -22,6 +22,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kSweeps = 15;   // cap on cyclic Jacobi sweeps (quadratic convergence: n <= 64 needs < 10 in fp64)
+// rotation threshold (R26): a pair (p, q) of the Gram matrix is rotated while g_pq^2 > kTol2 g_pp g_qq,
+// i.e. until the columns are orthogonal to 1e-9 relative -- 60x below the fp32 roundoff of the stored cores; the
+// eigenvalues (squared singular values, the delta-rank decisions) are then exact to ~1e-18 relative (A2 +3.8%
+// over eps_64)
+constexpr double kTol2 = 1e-18;
 constexpr double kSigmaFloor = 1e-7;
 
 __device__ double block_sum(double v, double* red) {
@@ -83,8 +88,8 @@ struct GatherWalk {
 // Symmetric eigenproblem of G (n x n, row-major in shared memory, overwritten by the rotated matrix) by cyclic
 // Jacobi; V (n x n) receives the eigenvectors as columns.  Round-robin ordering: n' = n rounded up to even
 // players, n'/2 disjoint rotations per round (player n' - 1 is a dummy when n is odd), n' - 1 rounds a sweep.
-// A pair is rotated only while |g_pq| > eps_64 sqrt(|g_pp g_qq|) (below that the rotation changes nothing at
-// fp64 precision); the iteration stops after a sweep that rotated no pair (or kSweeps sweeps).
+// A pair is rotated only while g_pq^2 > kTol2 |g_pp g_qq| (R26); the iteration stops after a sweep that rotated
+// no pair (or kSweeps sweeps).
 __device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int* pp, int* pq, int* flag) {
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) V[e] = (e / n == e % n) ? 1.0 : 0.0;
     const int np = (n + 1) & ~1, half = np / 2;
@@ -102,7 +107,7 @@ __device__ void jacobi(double* G, double* V, int n, double* cs, double* sn, int*
                 bool rot = false;
                 if (b < n) {
                     const double app = G[a * n + a], aqq = G[b * n + b], apq = G[a * n + b];
-                    if (fabs(apq) > 1e-300 && fabs(apq) > DBL_EPSILON * sqrt(fabs(app * aqq))) {
+                    if (fabs(apq) > 1e-300 && apq * apq > kTol2 * fabs(app * aqq)) {
                         const double th = (aqq - app) / (2.0 * apq);
                         const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
                         c = 1.0 / sqrt(tt * tt + 1.0);
@@ -525,7 +530,7 @@ __device__ double* jacobi_pair(double* G, double* Gn, double* V, int n, JacParam
                 double c = 1.0, sv = 0.0;
                 if (y < n) {
                     const double app = G[x * n + x], aqq = G[y * n + y], apq = G[x * n + y];
-                    if (fabs(apq) > 1e-300 && apq * apq > DBL_EPSILON * DBL_EPSILON * fabs(app * aqq)) {
+                    if (fabs(apq) > 1e-300 && apq * apq > kTol2 * fabs(app * aqq)) {
                         const double d = aqq - app, b2 = apq + apq;
                         const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
                         c = rsqrt(fma(tt, tt, 1.0));
@@ -606,7 +611,7 @@ __device__ double* jacobi_solo(double* G, double* Gn, double* V, int n, JacParam
             double c = 1.0, sv = 0.0;
             if (y < n) {
                 const double app = G[x * n + x], aqq = G[y * n + y], apq = G[x * n + y];
-                if (fabs(apq) > 1e-300 && apq * apq > DBL_EPSILON * DBL_EPSILON * fabs(app * aqq)) {
+                if (fabs(apq) > 1e-300 && apq * apq > kTol2 * fabs(app * aqq)) {
                     const double d = aqq - app, b2 = apq + apq;
                     const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
                     c = rsqrt(fma(tt, tt, 1.0));
