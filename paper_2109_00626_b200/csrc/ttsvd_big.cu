@@ -9,8 +9,8 @@
 //            (A V)^T = U^T Z = S V'^T, the next unfolding, directly.
 //   m >  c:  A = Z   (m x c).  Z V = U S  =>  U = columns of Z V / sigma, next unfolding S V^T.
 // Rotations of column pairs in the parallel round-robin order, until a sweep rotates nothing
-// (|a_p . a_q| <= max(1e-15, sqrt(L) eps) sqrt(|a_p|^2 |a_q|^2)); singular values = norms of A V's columns.  The delta-truncated
-// rank, the 1e-7 singular-value floor (R25) and the sign convention (R24: the largest-magnitude entry of every
+// (|a_p . a_q| <= 1e-9 sqrt(|a_p|^2 |a_q|^2), R26); singular values = norms of A V's columns.  The
+// delta-truncated rank, the 1e-7 singular-value floor (R25) and the sign convention (R24: the largest-magnitude entry of every
 // left singular vector positive, the matching row of S V^T flipped with it) are Alg. 1's as the oracle reads
 // them (oracle/ttsvd.py).  Alg. 2 step 1's permutation is folded into the first read.
 //
