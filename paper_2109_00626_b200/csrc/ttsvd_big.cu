@@ -39,6 +39,7 @@ constexpr int kRegCol = 16;            // warp-per-pair columns up to 32 kRegCol
 constexpr int kMaxBlk2 = 32;           // block mode: at most 2 x 16 columns per block pair
 constexpr int kLocalSweeps = 1;        // block mode: full local sweeps in a sweep's first block round
 constexpr int kDynBytes = 200 * 1024;  // block mode: dynamic shared memory per CTA
+static_assert(kBigWarps >= kMaxBlk2 / 2, "block mode: one warp per column pair of a full block round");
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
